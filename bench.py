@@ -1,0 +1,385 @@
+"""ALTO MTTKRP benchmark on B200 (driver contract: one JSON line from rank 0).
+
+Workload (BASELINE.json configs[1], "cfg2"): 3-mode 200,000 x 150,000 x
+100,000 tensor, 50M distinct nonzeros, Zipf(1.1) per mode, fp32 values,
+rank-16 fp32 factors; one step = MTTKRP over all 3 modes (streaming kernel).
+Metric: MTTKRP nonzeros/s (mode-averaged: 3*nnz per step / step time).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1 (torchrun): nonzeros are sharded by linearized-key range (ALTO
+partitions), factors replicated; each step adds an NCCL all-reduce of every
+mode's output (the shared-row exchange at its simplest), timed as the max
+over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def bytes_alg(dims, nnz, key_bytes, val_bytes, rank, fbytes, mode):
+    """M(K+V) + sum_{m!=n} I_m R S + I_n R S."""
+    return nnz * (key_bytes + val_bytes) + sum(d * rank * fbytes for d in dims)
+
+
+def cpu_baseline_sample(cfg_id: int, sample_nnz: int, threads: int, reps: int = 3):
+    """The reference algorithm (oracle port of mttkrp_par, Buffered = the
+    reference's auto choice for cfg2) on a bounded same-law sample, all modes."""
+    from oracle import alto_oracle as orc
+    from paper_2102_10245_b200 import synth
+
+    st = synth.make_tensor(cfg_id, nnz=sample_nnz)
+    c = st.config
+    lay = orc.build_layout(c.dims)
+    words, vals = orc.build(lay, st.coords, st.values.astype(np.float64))
+    rng = np.random.default_rng(synth.SEED_FACTOR_BASE + cfg_id)
+    factors = [rng.random((d, c.rank)).astype(np.float32).astype(np.float64) for d in c.dims]
+    offs, iv, _ = orc.partition(lay, words, threads)
+    times = []
+    for _rep in range(reps + 1):
+        t0 = time.perf_counter()
+        for mode in range(len(c.dims)):
+            orc.mttkrp_buffered(lay, words, vals, factors, mode, offs, iv, workers=threads)
+        times.append(time.perf_counter() - t0)
+    t = sum(times[1:]) / reps  # first rep is warm-up (cli.py:198-203 protocol)
+    return {"value": len(c.dims) * sample_nnz / t, "unit": "nnz/s", "cores": threads, "kind": "port",
+            "sample": f"{sample_nnz} nnz drawn from the {c.name} law (same dims, Zipf(1.1), fp32-rounded values), "
+                      f"all {len(c.dims)} modes, Buffered mttkrp_par over {threads} partitions/threads, "
+                      f"mean of {reps} after 1 warm-up",
+            "seconds_per_step": t}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    sample = args.cpu_sample
+    from oracle import alto_oracle as orc
+    from paper_2102_10245_b200 import synth
+
+    st = synth.make_tensor(args.config, nnz=sample)
+    c = st.config
+    lay = orc.build_layout(c.dims)
+    words, vals = orc.build(lay, st.coords, st.values.astype(np.float64))
+    rng = np.random.default_rng(synth.SEED_FACTOR_BASE + args.config)
+    factors = [rng.random((d, c.rank)).astype(np.float32).astype(np.float64) for d in c.dims]
+    offs, iv, _ = orc.partition(lay, words, threads)
+
+    def step():
+        for mode in range(len(c.dims)):
+            orc.mttkrp_buffered(lay, words, vals, factors, mode, offs, iv, workers=threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    t = (time.perf_counter() - t0) / args.steps
+    value = len(c.dims) * sample / t
+    line = {
+        "impl": "reference", "metric": "MTTKRP nonzeros/sec (mode-averaged)", "value": value, "unit": "nnz/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json law)",
+        "config": {"workload": f"{c.name}: dims {list(c.dims)}, Zipf(1.1), rank {c.rank}; CPU sample {sample} nnz",
+                   "sample_nnz": sample, "threads": threads},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} nnz of the {c.name} law, all modes, oracle port of the reference "
+                                   f"mttkrp_par (Buffered, {threads} workers)"},
+        "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2102_10245_b200 as at
+    from paper_2102_10245_b200 import synth
+    from paper_2102_10245_b200.format import AltoTensor, build_alto_device
+    from paper_2102_10245_b200.layout import build_masks
+    from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    nnz_total = args.nnz or cfg.nnz
+    t_gen = time.time()
+    st = synth.make_tensor(args.config, nnz=nnz_total)
+    t_gen = time.time() - t_gen
+    dims = cfg.dims
+    R = cfg.rank
+    lay = build_masks(dims)
+    # ALTO build on device (whole tensor), then keep this rank's key-range shard
+    coords = torch.from_numpy(st.coords).to(dev)
+    vdt = torch.float32 if cfg.value_dtype == "float32" else torch.float64
+    vals = torch.from_numpy(st.values).to(device=dev, dtype=vdt)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    full = build_alto_device(lay, coords, vals)
+    e1.record()
+    torch.cuda.synchronize()
+    build_ms = e0.elapsed_time(e1)
+    del coords, vals
+    if ws > 1:
+        offs = at.format.partition_offsets(full.nnz, ws)
+        a, b = int(offs[rank]), int(offs[rank + 1])
+        alto = AltoTensor(lay, full.keys[a:b].clone(), full.vals[a:b].clone())
+        del full
+    else:
+        alto = full
+    M = alto.nnz
+    fdt = np.float32 if cfg.value_dtype == "float32" else np.float64
+    rng = np.random.default_rng(synth.SEED_FACTOR_BASE + args.config)
+    factors_host = [rng.random((d, R)).astype(fdt) for d in dims]
+    fdev = factors_to_device(factors_host)
+    outs = [torch.empty((d, R), dtype=torch.float64, device=dev) for d in dims]
+    l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    N = len(dims)
+
+    def step(ev=None):
+        for mode in range(N):
+            if ev is not None:
+                ev[mode][0].record(stream)
+            mttkrp_stream(alto, fdev, mode, out=outs[mode], tile=args.tile)
+            if ev is not None:
+                ev[mode][1].record(stream)
+            if ws > 1:
+                dist.all_reduce(outs[mode])
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    # timed region: per-step events (L2 flushed before each step, outside the events)
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+    mode_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(N)]
+               for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush_l2(l2)
+            step_ev[k][0].record(stream)
+            step(mode_ev[k])
+            step_ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in step_ev]
+    ms = sum(step_ms) / len(step_ms)
+    mode_ms = [sum(mode_ev[k][n][0].elapsed_time(mode_ev[k][n][1]) for k in range(args.steps)) / args.steps
+               for n in range(N)]
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms_max = float(t_ms.item())
+    value = N * nnz_total / (ms_max * 1e-3)
+
+    # roofline of the dominant kernel (the streaming MTTKRP), per mode
+    peak, peak_kind = measured_peaks()
+    kb, vb, fb = 8 * lay.n_words, 4 if vdt == torch.float32 else 8, np.dtype(fdt).itemsize
+    per_mode = []
+    for n in range(N):
+        ba = bytes_alg(dims, M, kb, vb, R, fb, n)
+        per_mode.append({"mode": n, "kernel_ms": mode_ms[n], "bytes_alg": ba,
+                         "achieved_gbs": ba / (mode_ms[n] * 1e-3) / 1e9,
+                         "nnz_per_s": M / (mode_ms[n] * 1e-3)})
+    tot_b = sum(p["bytes_alg"] for p in per_mode)
+    tot_t = sum(mode_ms) * 1e-3
+    achieved = tot_b / tot_t / 1e9
+
+    # end-to-end through the reference-facing API: mttkrp_par with an Atomic plan
+    # (the CLI protocol: prepare once, cli.py:194; per step host factors in,
+    # float64 result out, cli.py:198-203)
+    parts = at.partition(alto, 8)
+    plans, flagged = [], []
+    for n in range(N):
+        p = at.plan_conflicts(alto, parts, n, force_strategy=at.Strategy.ATOMIC)
+        plans.append(p)
+        flagged.append(at.apply_boundary_flags(alto, p) if p.flag_bit is not None else alto)
+    fpin = [torch.from_numpy(f).pin_memory() for f in factors_host]
+    opin = [torch.empty((d, R), dtype=torch.float64).pin_memory() for d in dims]
+
+    def e2e_step():
+        for n in range(N):
+            o = at.mttkrp_par(flagged[n], parts, plans[n], fpin, n, workers=1)
+            opin[n].copy_(o, non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    ee1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = ee0.elapsed_time(ee1) / args.steps
+    t_e = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t_e.item())
+    h2d = N * sum(d * R * fb for d in dims)
+    d2h = sum(d * R * 8 for d in dims)
+
+    # CP-ALS iteration time (device loop, streaming backend), single GPU only
+    cpals = None
+    if ws == 1 and not args.skip_cpals:
+        from paper_2102_10245_b200.cpd import DeviceCpAls
+
+        st_als = DeviceCpAls(alto, R, seed=0, backend="atomic", partitions=8)
+        st_als.sweep()
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        iters = 3
+        for _ in range(iters):
+            st_als.sweep()
+        c1.record(stream)
+        torch.cuda.synchronize()
+        cpals = c0.elapsed_time(c1) / iters
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.skip_cpu:
+        cpu = cpu_baseline_sample(args.config, args.cpu_sample, len(os.sched_getaffinity(0)))
+
+    if rank == 0:
+        line = {
+            "metric": "MTTKRP nonzeros/sec (mode-averaged)",
+            "value": value, "unit": "nnz/s", "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; BASELINE.json cfg2 law)",
+            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, dims))}, {nnz_total} nnz, Zipf(1.1) all modes, "
+                                   f"fp32 values, rank {R}; step = MTTKRP all {N} modes",
+                       "nnz": nnz_total, "rank": R, "tile": args.tile, "key_bits": lay.total_bits,
+                       "l2": "flushed (256 MB write) before every timed step; keys+values "
+                             f"{M * (kb + vb) / 1e6:.0f} MB > 126 MB L2",
+                       "parallelism": f"key-range shards x{ws}" if ws > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_kind,
+                         "traffic": None, "kernel": "mttkrp_tile_kernel", "per_mode": per_mode},
+            "e2e": {"value": N * nnz_total / (e2e_ms * 1e-3), "unit": "nnz/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "api": "paper_2102_10245_b200.mttkrp_par (Atomic plan) with pinned host fp32 factors in, "
+                           "float64 result copied to pinned host memory, every mode"},
+            "gpu_launches": args.steps * N,
+            "clocks": clk.summary(),
+            "build_ms": build_ms, "gen_s": t_gen,
+            "cpals_ms_per_iter": cpals,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--nnz", type=int, default=0, help="override nnz (testing)")
+    ap.add_argument("--tile", type=int, default=1024)
+    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-cpals", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,221 @@
+/*
+ * alto_b200.h — C ABI of the B200-native ALTO hot path (libalto_b200.so).
+ *
+ * The reference (arXiv 2102.10245, package `altotensor`, /root/reference/pkg)
+ * is pure Python: its boundary is the Python API in
+ * pkg/src/altotensor/__init__.py:9-92, not an FFI.  Every entry point below
+ * replaces the arithmetic of one reference function (cited per function); the
+ * Python package paper_2102_10245_b200 binds them with ctypes and keeps the
+ * reference signatures on top.
+ *
+ * Conventions
+ *   - extern "C"; plain pointers, element counts, and a cudaStream_t passed as
+ *     `void*` (NULL = legacy default stream).  No torch types.
+ *   - All data pointers are DEVICE pointers unless the name says `host`.
+ *   - The caller owns every buffer.  Scratch memory is passed in as a
+ *     caller-allocated workspace whose size comes from a *_workspace_bytes()
+ *     query.  The library never allocates or frees caller memory.
+ *   - Calls are stream-ordered and asynchronous unless documented otherwise.
+ *   - Return status: ALTO_OK, or an ALTO_E* code; alto_last_error() returns a
+ *     thread-local message for the last failing call.
+ *   - Keys ("indices" in the reference) are stored as n_words little-endian
+ *     uint64 per element, least-significant word first, array-of-structs
+ *     ((nnz, n_words) row-major), exactly like pkg/src/altotensor/layout.py:151.
+ */
+#ifndef ALTO_B200_H
+#define ALTO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ALTO_MAX_ORDER 8
+#define ALTO_MAX_BITS 128
+
+enum alto_status {
+  ALTO_OK = 0,
+  ALTO_EINVAL = 1,     /* invalid argument -> Python ValueError            */
+  ALTO_ECUDA = 2,      /* CUDA runtime error                               */
+  ALTO_EUNSUPPORTED = 3,
+  ALTO_ENCCL = 4,
+  ALTO_ESINGULAR = 5   /* normal equations singular -> np.linalg.LinAlgError */
+};
+
+enum alto_dtype { ALTO_F32 = 0, ALTO_F64 = 1 };
+
+/* Bit layout of the linearized index (pkg/src/altotensor/layout.py:38-71).
+ * Filled on the host from AltoLayout.positions; pos[n][g] is the key bit
+ * holding bit g of mode n. */
+typedef struct alto_layout {
+  int32_t order;                     /* N                                   */
+  int32_t n_words;                   /* 1 (width 64) or 2 (width 128)       */
+  int32_t total_bits;                /* sum of bits[]                       */
+  int32_t width;                     /* 64 or 128                           */
+  int64_t dims[ALTO_MAX_ORDER];
+  int32_t bits[ALTO_MAX_ORDER];
+  uint8_t pos[ALTO_MAX_ORDER][64];
+} alto_layout;
+
+const char* alto_last_error(void);
+int alto_version(void);
+
+/* Size in bytes of the device-resident encode/decode tables for a layout
+ * (byte-indexed deposit tables per mode, byte-indexed extract tables per key
+ * byte).  alto_build_tables fills a caller-allocated device buffer of that
+ * size (synchronous host->device copy of host-computed tables). */
+size_t alto_tables_bytes(const alto_layout* lay);
+int alto_build_tables(const alto_layout* lay, void* d_tables, void* stream);
+
+/* K1 — linearize_array (layout.py:148-160, range check layout.py:135-145).
+ * coords: (M, order) int64 row-major.  keys: (M, n_words) uint64.
+ * *d_bad (device int64, caller-zeroed to -1 beforehand is NOT required: the
+ * call resets it) receives the lowest row index holding an out-of-range
+ * coordinate, or -1. */
+int alto_linearize(const alto_layout* lay, const void* d_tables,
+                   const int64_t* coords, int64_t m, uint64_t* keys,
+                   int64_t* d_bad, void* stream);
+
+/* K4 — extract_mode_array / delinearize_array (layout.py:163-182).
+ * mode >= 0: out is (M,) int64 for that mode; mode == -1: out is (M, order).
+ * Bits above total_bits (flags) are ignored (layout.py:125). */
+int alto_delinearize(const alto_layout* lay, const void* d_tables,
+                     const uint64_t* keys, int64_t m, int32_t mode,
+                     int64_t* out, void* stream);
+
+/* K2 — stable LSD radix sort of (keys, payload) over key bits
+ * [0, total_bits): replaces np.lexsort + co-permutation (format.py:79-82,
+ * :94-97).  payload_bytes in {0, 4, 8}.  Result lands in keys/payload. */
+size_t alto_sort_workspace_bytes(int64_t m, int32_t n_words, int32_t payload_bytes);
+int alto_sort_pairs(uint64_t* keys, void* payload, int64_t m, int32_t n_words,
+                    int32_t payload_bytes, int32_t total_bits, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* K3 — duplicate check (format.py:98-99): *d_first = lowest i>0 with
+ * key[i] == key[i-1] over all words, or -1. */
+int alto_find_duplicate(const uint64_t* keys, int64_t m, int32_t n_words,
+                        int64_t* d_first, void* stream);
+
+/* K5 — partition (format.py:127-154).  Equal-nnz ranges, larger first
+ * (format.py:136-140).  intervals: (count, order, 2) int64, per-partition
+ * min/max of every mode, (0,-1) for empty partitions (format.py:146-149).
+ * spans: (count, 2, n_words) uint64 first/last key of each partition (empty
+ * partitions left untouched). */
+int alto_partition(const alto_layout* lay, const void* d_tables,
+                   const uint64_t* keys, int64_t m, int64_t count,
+                   int64_t* intervals, uint64_t* spans, void* stream);
+
+/* K6 — apply_boundary_flags (format.py:257-285): out_keys = keys with bit
+ * flag_bit set on every element whose `mode` coordinate lies in one of its
+ * partition's overlap ranges.  Overlaps in CSR form: partition l owns ranges
+ * [ov_ptr[l], ov_ptr[l+1]) of (ov_lo[], ov_hi[]), ascending and disjoint. */
+int alto_apply_flags(const alto_layout* lay, const void* d_tables,
+                     const uint64_t* keys, int64_t m, int64_t count,
+                     int32_t mode, int32_t flag_bit, const int64_t* ov_ptr,
+                     const int64_t* ov_lo, const int64_t* ov_hi,
+                     uint64_t* out_keys, void* stream);
+/* read_flags / clear_flags (format.py:288-299). */
+int alto_read_flags(const uint64_t* keys, int64_t m, int32_t n_words,
+                    int32_t flag_bit, uint8_t* out, void* stream);
+int alto_clear_flags(const uint64_t* keys, int64_t m, int32_t n_words,
+                     int32_t flag_bit, uint64_t* out_keys, void* stream);
+
+/* ---- MTTKRP (mttkrp.py) ------------------------------------------------ */
+
+/* Per-mode device plan for the streaming kernel: the sorted stream is cut
+ * into tiles of `tile` elements; for each tile the mode-`mode` interval is
+ * recorded (tile_lo/tile_hi, int32 each, (ntiles,)). */
+int64_t alto_mttkrp_ntiles(int64_t m, int32_t tile);
+int alto_tile_intervals(const alto_layout* lay, const void* d_tables,
+                        const uint64_t* keys, int64_t m, int32_t tile,
+                        int32_t* tile_lo /* (ntiles, order) */,
+                        int32_t* tile_hi /* (ntiles, order) */, void* stream);
+
+typedef struct alto_mttkrp_args {
+  const alto_layout* lay;
+  const void* d_tables;
+  const uint64_t* keys;          /* (M, n_words) */
+  const void* values;            /* (M,) value_dtype */
+  int64_t m;
+  int32_t mode;
+  int32_t rank;
+  int32_t value_dtype;           /* ALTO_F32 / ALTO_F64 */
+  int32_t factor_dtype;          /* ALTO_F32 / ALTO_F64 */
+  const void* factors[ALTO_MAX_ORDER]; /* (I_n, rank) row-major, factor_dtype */
+  double* out;                   /* (I_mode, rank) float64, accumulated into */
+  int32_t tile;                  /* elements per tile (plan granularity)   */
+  const int32_t* tile_lo;        /* (ntiles, order) from alto_tile_intervals */
+  const int32_t* tile_hi;
+  int32_t zero_out;              /* 1: out is zeroed first (stream-ordered) */
+} alto_mttkrp_args;
+
+/* K7/K8 — streaming ALTO MTTKRP (mttkrp.py:80-105 contributions,
+ * :132-224 conflict resolution).  Each CTA owns a tile of the sorted stream;
+ * tiles whose output-mode interval fits on chip accumulate in shared memory
+ * and push one fp64 update per touched row (per-tile interval buffer + merge,
+ * the Buffered scheme); wider tiles push fp64 atomics per element (Atomic
+ * scheme).  Output is float64 like the reference (mttkrp.py:144, :202). */
+int alto_mttkrp(const alto_mttkrp_args* a, void* stream);
+
+/* Exact-order engine (deterministic; bitwise equal to the reference for
+ * float64 data): for mode `mode`, `row_perm` lists element indices sorted by
+ * (mode coordinate, element index) and `row_ptr` (I_mode+1) delimits rows.
+ * Partition boundaries `part_off` (count+1) split each row's sum, and the
+ * per-partition partials are combined in ascending partition order — the
+ * Buffered stage + pull of mttkrp.py:148-172 (count = 1 gives mttkrp_seq,
+ * mttkrp.py:108-117). */
+size_t alto_row_index_workspace_bytes(int64_t m, int64_t dim);
+int alto_row_index(const alto_layout* lay, const void* d_tables,
+                   const uint64_t* keys, int64_t m, int32_t mode,
+                   int32_t* row_perm /* (M,) */, int64_t* row_ptr /* (dim+1,) */,
+                   void* workspace, size_t workspace_bytes, void* stream);
+int alto_mttkrp_exact(const alto_mttkrp_args* a, const int32_t* row_perm,
+                      const int64_t* row_ptr, const int64_t* part_off,
+                      int64_t count, void* stream);
+
+/* COO MTTKRP over a coordinate list (mttkrp_oracle, mttkrp.py:64-77),
+ * coords (M, order) int64, float64 atomics. */
+int alto_mttkrp_coo(const int64_t* coords, const double* values, int64_t m,
+                    int32_t order, int32_t mode, int32_t rank,
+                    const double* const* factors_host_array /* host array of N device ptrs */,
+                    double* out, int64_t out_rows, void* stream);
+
+/* ---- CP-ALS (cpd.py) --------------------------------------------------- */
+/* All reductions below are two-stage with a fixed block count, so results
+ * are bitwise reproducible run to run (cpd_als determinism,
+ * pkg/tests/test_cpd.py:125-130).  `ws` is a caller workspace of at least
+ * alto_cpd_workspace_bytes(rank) bytes. */
+size_t alto_cpd_workspace_bytes(int32_t rank);
+
+/* K10 gram (cpd.py:66-68): G = F^T F accumulated in float64. F (rows, rank). */
+int alto_gram(const void* f, int32_t f_dtype, int64_t rows, int32_t rank, double* g,
+              void* ws, size_t ws_bytes, void* stream);
+/* K10 _hadamard_grams (cpd.py:71-77): V = 1 * prod over n != skip of G_n, in
+ * mode order (skip = -1: all).  grams_host_array: host array of `order`
+ * device pointers. */
+int alto_hadamard_grams(const double* const* grams_host_array, int32_t order, int32_t skip,
+                        int32_t rank, double* v, void* stream);
+/* K11 + K12 (cpd.py:80-95, :116-120): solve X V = M by Cholesky (retry once
+ * with ridge 1e-12 tr(V)/R), lambda = column 2-norms of X, X /= lambda
+ * (zero-safe).  Writes X (float64) to x64 and, when x32 != NULL, a float32
+ * copy.  *d_status (device int32): 0 ok, 1 ridge used, 2 singular. */
+int alto_solve_normalize(const double* v, const double* mttkrp, int64_t rows, int32_t rank,
+                         double* x64, float* x32, double* lambda, int32_t* d_status,
+                         void* ws, size_t ws_bytes, void* stream);
+/* K13 fit terms (cpd.py:124-146): out2[0] = sum_{i,r} M[i,r] F[i,r] lambda_r,
+ * out2[1] = lambda^T V_all lambda. */
+int alto_fit_terms(const double* mttkrp, const double* f, const double* lambda,
+                   const double* v_all, int64_t rows, int32_t rank, double* out2,
+                   void* ws, size_t ws_bytes, void* stream);
+/* sum of squares of values in float64 (cpd.py:211). */
+int alto_sumsq(const void* values, int32_t dtype, int64_t m, double* out,
+               void* ws, size_t ws_bytes, void* stream);
+/* Cast helpers for factor uploads: out32[i] = (float)in64[i]. */
+int alto_cast_f64_f32(const double* in, float* out, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ALTO_B200_H */

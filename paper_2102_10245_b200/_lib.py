@@ -1,0 +1,153 @@
+"""ctypes binding of libalto_b200.so (the C ABI declared in include/alto_b200.h).
+
+The shared library is built in-tree by `make` (or __graft_entry__.build()).
+There is no CPU fallback: if the library or a CUDA device is missing, the
+device entry points raise `RuntimeError` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import (POINTER, Structure, c_char_p, c_double, c_int32, c_int64,
+                    c_size_t, c_uint8, c_void_p)
+
+import numpy as np
+
+ALTO_MAX_ORDER = 8
+ALTO_OK, ALTO_EINVAL, ALTO_ECUDA, ALTO_EUNSUPPORTED, ALTO_ENCCL, ALTO_ESINGULAR = range(6)
+ALTO_F32, ALTO_F64 = 0, 1
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libalto_b200.so")
+
+
+class CLayout(Structure):
+    _fields_ = [
+        ("order", c_int32),
+        ("n_words", c_int32),
+        ("total_bits", c_int32),
+        ("width", c_int32),
+        ("dims", c_int64 * ALTO_MAX_ORDER),
+        ("bits", c_int32 * ALTO_MAX_ORDER),
+        ("pos", (c_uint8 * 64) * ALTO_MAX_ORDER),
+    ]
+
+
+class CMttkrpArgs(Structure):
+    _fields_ = [
+        ("lay", POINTER(CLayout)),
+        ("d_tables", c_void_p),
+        ("keys", c_void_p),
+        ("values", c_void_p),
+        ("m", c_int64),
+        ("mode", c_int32),
+        ("rank", c_int32),
+        ("value_dtype", c_int32),
+        ("factor_dtype", c_int32),
+        ("factors", c_void_p * ALTO_MAX_ORDER),
+        ("out", c_void_p),
+        ("tile", c_int32),
+        ("tile_lo", c_void_p),
+        ("tile_hi", c_void_p),
+        ("zero_out", c_int32),
+    ]
+
+
+# (name, restype, argtypes) for every symbol of include/alto_b200.h
+SIGNATURES = [
+    ("alto_last_error", c_char_p, []),
+    ("alto_version", c_int32, []),
+    ("alto_tables_bytes", c_size_t, [POINTER(CLayout)]),
+    ("alto_build_tables", c_int32, [POINTER(CLayout), c_void_p, c_void_p]),
+    ("alto_linearize", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    ("alto_delinearize", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    ("alto_sort_workspace_bytes", c_size_t, [c_int64, c_int32, c_int32]),
+    ("alto_sort_pairs", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_size_t,
+                                  c_void_p]),
+    ("alto_find_duplicate", c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    ("alto_partition", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p,
+                                 c_void_p]),
+    ("alto_apply_flags", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int64, c_int32, c_int32,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("alto_read_flags", c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
+    ("alto_clear_flags", c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
+    ("alto_mttkrp_ntiles", c_int64, [c_int64, c_int32]),
+    ("alto_tile_intervals", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
+                                      c_void_p]),
+    ("alto_mttkrp", c_int32, [POINTER(CMttkrpArgs), c_void_p]),
+    ("alto_row_index_workspace_bytes", c_size_t, [c_int64, c_int64]),
+    ("alto_row_index", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
+                                 c_void_p, c_size_t, c_void_p]),
+    ("alto_mttkrp_exact", c_int32, [POINTER(CMttkrpArgs), c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+    ("alto_mttkrp_coo", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, POINTER(c_void_p),
+                                  c_void_p, c_int64, c_void_p]),
+    ("alto_cpd_workspace_bytes", c_size_t, [c_int32]),
+    ("alto_gram", c_int32, [c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("alto_hadamard_grams", c_int32, [POINTER(c_void_p), c_int32, c_int32, c_int32, c_void_p, c_void_p]),
+    ("alto_solve_normalize", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("alto_fit_terms", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
+                                 c_size_t, c_void_p]),
+    ("alto_sumsq", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("alto_cast_f64_f32", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+]
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load the library (once) and bind every C ABI symbol."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(
+            f"libalto_b200.so not found at {p}; build it with `make` or __graft_entry__.build()"
+        )
+    lib = ctypes.CDLL(p)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+class AltoDeviceError(RuntimeError):
+    pass
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a C ABI status to the reference's exception types."""
+    if status == ALTO_OK:
+        return
+    msg = load().alto_last_error().decode(errors="replace")
+    if status == ALTO_EINVAL:
+        raise ValueError(msg)
+    if status == ALTO_ESINGULAR:
+        raise np.linalg.LinAlgError(msg)
+    raise AltoDeviceError(f"{what}: status {status}: {msg}")
+
+
+def cuda_device():
+    """The CUDA device the product path runs on; raises if there is none."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2102_10245_b200 needs a CUDA (B200) device; no CPU fallback exists")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()

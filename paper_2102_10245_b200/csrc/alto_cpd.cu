@@ -1,0 +1,355 @@
+// alto_cpd.cu — CP-ALS step on device (K10-K13), replacing the NumPy/SciPy
+// arithmetic of pkg/src/altotensor/cpd.py:66-146.
+//
+// Every reduction is two-stage over a FIXED number of blocks (kRedBlocks)
+// with a fixed in-block order, so results are bitwise reproducible from run
+// to run, which cpd_als's seed-determinism contract needs
+// (pkg/tests/test_cpd.py:125-130).  All arithmetic is float64 (SURVEY §7.3
+// item 9: fit parity needs float64 norms and Cholesky even for fp32 data).
+#include <cmath>
+
+#include "alto_common.cuh"
+
+namespace alto {
+
+constexpr int kRedBlocks = 256;
+constexpr int kRedThreads = 256;
+constexpr int kMaxRank = 64;
+
+// ---- K10 gram ---------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) gram_partial(const T* __restrict__ f, long long rows, int R,
+                                                            double* __restrict__ part) {
+  __shared__ double s_f[32][kMaxRank + 1];
+  const long long chunk = (rows + gridDim.x - 1) / gridDim.x;
+  const long long r0 = blockIdx.x * chunk;
+  const long long r1 = min(rows, r0 + chunk);
+  const int RR = R * R;
+  double acc[(kMaxRank * kMaxRank + kRedThreads - 1) / kRedThreads];
+  const int per = (RR + kRedThreads - 1) / kRedThreads;
+  for (int q = 0; q < per; ++q) acc[q] = 0.0;
+  for (long long base = r0; base < r1; base += 32) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < 32 * R; t += blockDim.x) {
+      const int k = t / R, c = t - k * R;
+      const long long row = base + k;
+      s_f[k][c] = row < r1 ? static_cast<double>(f[row * R + c]) : 0.0;
+    }
+    __syncthreads();
+    const int nk = static_cast<int>(min(32ll, r1 - base));
+    for (int q = 0; q < per; ++q) {
+      const int idx = threadIdx.x + q * kRedThreads;
+      if (idx < RR) {
+        const int i = idx / R, j = idx - (idx / R) * R;
+        double a = acc[q];
+        for (int k = 0; k < nk; ++k) a = fma(s_f[k][i], s_f[k][j], a);
+        acc[q] = a;
+      }
+    }
+  }
+  for (int q = 0; q < per; ++q) {
+    const int idx = threadIdx.x + q * kRedThreads;
+    if (idx < RR) part[static_cast<long long>(blockIdx.x) * RR + idx] = acc[q];
+  }
+}
+
+__global__ void sum_partials(const double* __restrict__ part, int nblocks, int width, double* __restrict__ out) {
+  for (int idx = threadIdx.x; idx < width; idx += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += part[static_cast<long long>(b) * width + idx];
+    out[idx] = s;
+  }
+}
+
+struct GramPtrs {
+  const double* g[ALTO_MAX_ORDER];
+};
+
+__global__ void hadamard_kernel(const __grid_constant__ GramPtrs G, int order, int skip, int RR,
+                                double* __restrict__ v) {
+  for (int idx = threadIdx.x; idx < RR; idx += blockDim.x) {
+    double x = 1.0;
+    for (int n = 0; n < order; ++n)
+      if (n != skip) x = __dmul_rn(x, G.g[n][idx]);
+    v[idx] = x;
+  }
+}
+
+// ---- K11 Cholesky + ridge retry ------------------------------------------------
+
+__device__ bool cholesky_lower(double* a, int R) {
+  // In place, lower triangle; a is R x R row-major in shared memory.
+  for (int j = 0; j < R; ++j) {
+    double d = a[j * R + j];
+    for (int k = 0; k < j; ++k) d -= a[j * R + k] * a[j * R + k];
+    if (!(d > 0.0) || !isfinite(d)) return false;
+    const double l = sqrt(d);
+    a[j * R + j] = l;
+    for (int i = j + 1; i < R; ++i) {
+      double s = a[i * R + j];
+      for (int k = 0; k < j; ++k) s -= a[i * R + k] * a[j * R + k];
+      a[i * R + j] = s / l;
+    }
+  }
+  return true;
+}
+
+__global__ void cholesky_kernel(const double* __restrict__ v, int R, double* __restrict__ lout,
+                                int* __restrict__ status) {
+  __shared__ double s_a[kMaxRank * kMaxRank];
+  if (threadIdx.x != 0) return;
+  bool finite = true;
+  double tr = 0.0;
+  if (*status == 2) return;
+  for (int i = 0; i < R * R; ++i) {
+    s_a[i] = v[i];
+    finite &= static_cast<bool>(isfinite(v[i]));
+  }
+  for (int i = 0; i < R; ++i) tr += v[i * R + i];
+  int st = 0;
+  if (!(finite && cholesky_lower(s_a, R))) {
+    // ridge retry (cpd.py:87-91)
+    const double ridge = 1e-12 * tr / R;
+    for (int i = 0; i < R * R; ++i) s_a[i] = v[i];
+    for (int i = 0; i < R; ++i) s_a[i * R + i] += ridge;
+    st = (finite && isfinite(ridge) && cholesky_lower(s_a, R)) ? 1 : 2;
+  }
+  for (int i = 0; i < R * R; ++i) lout[i] = s_a[i];
+  // sticky: a singular solve earlier in the stream stays visible until the
+  // host checks (later solves on a poisoned stream are skipped)
+  if (st > *status) *status = st;
+}
+
+// Row solve x V = m  <=>  L (L^T x^T) = m^T, plus per-block column sum of squares.
+__global__ void __launch_bounds__(kRedThreads) solve_rows(const double* __restrict__ lmat,
+                                                          const double* __restrict__ mt, long long rows, int R,
+                                                          double* __restrict__ x64,
+                                                          const int* __restrict__ status,
+                                                          double* __restrict__ part) {
+  __shared__ double s_l[kMaxRank * kMaxRank];
+  __shared__ double s_sq[kRedThreads / 32][kMaxRank];
+  if (*status == 2) return;
+  for (int i = threadIdx.x; i < R * R; i += blockDim.x) s_l[i] = lmat[i];
+  __syncthreads();
+  const long long chunk = (rows + gridDim.x - 1) / gridDim.x;
+  const long long r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
+  double sq[kMaxRank];
+  for (int c = 0; c < R; ++c) sq[c] = 0.0;
+  for (long long row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
+    double y[kMaxRank];
+    for (int i = 0; i < R; ++i) {
+      double s = mt[row * R + i];
+      for (int k = 0; k < i; ++k) s -= s_l[i * R + k] * y[k];
+      y[i] = s / s_l[i * R + i];
+    }
+    for (int i = R - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < R; ++k) s -= s_l[k * R + i] * y[k];
+      y[i] = s / s_l[i * R + i];
+    }
+    for (int c = 0; c < R; ++c) {
+      x64[row * R + c] = y[c];
+      sq[c] += y[c] * y[c];
+    }
+  }
+  // fixed-order block reduction of sq
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = 0; c < R; ++c) {
+    double s = sq[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) s_sq[warp][c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) s += s_sq[w][threadIdx.x];
+    part[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = s;
+  }
+}
+
+__global__ void lambda_kernel(const double* __restrict__ part, int nblocks, int R, double* __restrict__ lambda,
+                              const int* __restrict__ status) {
+  if (*status == 2) return;
+  for (int c = threadIdx.x; c < R; c += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += part[static_cast<long long>(b) * R + c];
+    lambda[c] = sqrt(s);
+  }
+}
+
+__global__ void normalize_kernel(double* __restrict__ x64, float* __restrict__ x32, long long rows, int R,
+                                 const double* __restrict__ lambda, const int* __restrict__ status) {
+  if (*status == 2) return;
+  const long long n = rows * R;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const int c = static_cast<int>(i % R);
+    const double w = lambda[c];
+    const double x = x64[i] / (w == 0.0 ? 1.0 : w);
+    x64[i] = x;
+    if (x32) x32[i] = static_cast<float>(x);
+  }
+}
+
+// ---- K13 fit terms / norms ---------------------------------------------------------
+
+__device__ __forceinline__ double block_sum_fixed(double v, double* s_tmp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) s_tmp[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += s_tmp[w];
+  return s;
+}
+
+__global__ void __launch_bounds__(kRedThreads) inner_partial(const double* __restrict__ mt,
+                                                             const double* __restrict__ f,
+                                                             const double* __restrict__ lambda, long long rows,
+                                                             int R, double* __restrict__ part) {
+  __shared__ double s_tmp[32];
+  const long long n = rows * R;
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  double s = 0.0;
+  for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) s += (mt[i] * f[i]) * lambda[i % R];
+  s = block_sum_fixed(s, s_tmp);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void fit_final(const double* __restrict__ part, int nblocks, const double* __restrict__ lambda,
+                          const double* __restrict__ vall, int R, double* __restrict__ out2) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int b = 0; b < nblocks; ++b) s += part[b];
+  out2[0] = s;
+  double q = 0.0;
+  for (int j = 0; j < R; ++j) {
+    double u = 0.0;
+    for (int i = 0; i < R; ++i) u += lambda[i] * vall[i * R + j];
+    q += u * lambda[j];
+  }
+  out2[1] = q;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) sumsq_partial(const T* __restrict__ v, long long n,
+                                                             double* __restrict__ part) {
+  __shared__ double s_tmp[32];
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  double s = 0.0;
+  for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const double x = static_cast<double>(v[i]);
+    s += x * x;
+  }
+  s = block_sum_fixed(s, s_tmp);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void sum_scalar(const double* __restrict__ part, int nblocks, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int b = 0; b < nblocks; ++b) s += part[b];
+  *out = s;
+}
+
+__global__ void cast_kernel(const double* __restrict__ in, float* __restrict__ out, long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    out[i] = static_cast<float>(in[i]);
+}
+
+static size_t cpd_ws_doubles(int R) {
+  return static_cast<size_t>(kRedBlocks) * R * R + static_cast<size_t>(R) * R + 64;
+}
+
+}  // namespace alto
+
+using namespace alto;
+
+extern "C" {
+
+size_t alto_cpd_workspace_bytes(int32_t rank) {
+  if (rank < 1) rank = 1;
+  return cpd_ws_doubles(rank) * sizeof(double);
+}
+
+int alto_gram(const void* f, int32_t f_dtype, int64_t rows, int32_t rank, double* g, void* ws, size_t ws_bytes,
+              void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  if (f_dtype == ALTO_F32)
+    gram_partial<float><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const float*>(f), rows, rank, part);
+  else
+    gram_partial<double><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const double*>(f), rows, rank, part);
+  sum_partials<<<1, 256, 0, s>>>(part, kRedBlocks, rank * rank, g);
+  ALTO_LAUNCH_CHECK("alto_gram");
+  return ALTO_OK;
+}
+
+int alto_hadamard_grams(const double* const* grams_host_array, int32_t order, int32_t skip, int32_t rank, double* v,
+                        void* stream) {
+  ALTO_REQUIRE(order >= 1 && order <= ALTO_MAX_ORDER, "order out of range");
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  GramPtrs G{};
+  for (int n = 0; n < order; ++n) G.g[n] = grams_host_array[n];
+  hadamard_kernel<<<1, 256, 0, as_stream(stream)>>>(G, order, skip, rank * rank, v);
+  ALTO_LAUNCH_CHECK("alto_hadamard_grams");
+  return ALTO_OK;
+}
+
+int alto_solve_normalize(const double* v, const double* mttkrp, int64_t rows, int32_t rank, double* x64, float* x32,
+                         double* lambda, int32_t* d_status, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  double* lmat = part + static_cast<size_t>(kRedBlocks) * rank * rank;
+  cholesky_kernel<<<1, 32, 0, s>>>(v, rank, lmat, d_status);
+  solve_rows<<<kRedBlocks, kRedThreads, 0, s>>>(lmat, mttkrp, rows, rank, x64, d_status, part);
+  lambda_kernel<<<1, 64, 0, s>>>(part, kRedBlocks, rank, lambda, d_status);
+  normalize_kernel<<<grid_for(rows * rank, 256), 256, 0, s>>>(x64, x32, rows, rank, lambda, d_status);
+  ALTO_LAUNCH_CHECK("alto_solve_normalize");
+  return ALTO_OK;
+}
+
+int alto_fit_terms(const double* mttkrp, const double* f, const double* lambda, const double* v_all, int64_t rows,
+                   int32_t rank, double* out2, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  inner_partial<<<kRedBlocks, kRedThreads, 0, s>>>(mttkrp, f, lambda, rows, rank, part);
+  fit_final<<<1, 32, 0, s>>>(part, kRedBlocks, lambda, v_all, rank, out2);
+  ALTO_LAUNCH_CHECK("alto_fit_terms");
+  return ALTO_OK;
+}
+
+int alto_sumsq(const void* values, int32_t dtype, int64_t m, double* out, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(ws && ws_bytes >= kRedBlocks * sizeof(double), "workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  if (dtype == ALTO_F32)
+    sumsq_partial<float><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const float*>(values), m, part);
+  else
+    sumsq_partial<double><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const double*>(values), m, part);
+  sum_scalar<<<1, 32, 0, s>>>(part, kRedBlocks, out);
+  ALTO_LAUNCH_CHECK("alto_sumsq");
+  return ALTO_OK;
+}
+
+int alto_cast_f64_f32(const double* in, float* out, int64_t n, void* stream) {
+  if (n <= 0) return ALTO_OK;
+  cast_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(in, out, n);
+  ALTO_LAUNCH_CHECK("alto_cast_f64_f32");
+  return ALTO_OK;
+}
+
+}  // extern "C"

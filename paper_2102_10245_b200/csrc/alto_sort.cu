@@ -1,0 +1,337 @@
+// alto_sort.cu — K2 hand-written stable LSD radix sort on linearized keys
+// (+ payload), K3 duplicate detection.
+//
+// Replaces np.lexsort over the index words with last word primary and the
+// co-permutation of values (format.py:79-82, :94-97).  Because keys occupy
+// only bits [0, total_bits), exactly ceil(total_bits/8) 8-bit digit passes
+// are run (4/7/9/6/9 passes for BASELINE cfg1..cfg5).
+//
+// One pass = three stream-ordered kernels:
+//   1. radix_hist   : per-tile digit histogram -> counts[digit * ntiles + tile]
+//   2. exclusive scan of counts (digit-major, so the scan yields the global
+//      destination of (digit, tile) directly)
+//   3. radix_scatter: stable in-tile ranking.  Each warp owns a contiguous
+//      512-key slice of the 4096-key tile, visited in index order
+//      (round j, lane l); __match_any_sync groups equal digits, the group's
+//      lower lanes give the rank, per-warp running digit counters carry the
+//      rank across rounds, and a per-digit exclusive scan over warps orders
+//      the warps.  dest = scan[digit, tile] + warp prefix + rank — stable.
+#include <climits>
+
+#include "alto_common.cuh"
+
+namespace alto {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kWarpSlice = kSortTile / kSortWarps;     // 512 keys per warp
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanChunk = kScanThreads * kScanItems;  // 4096 counters
+
+template <int W>
+__device__ __forceinline__ unsigned digit_of(const Key<W>& k, int shift) {
+  return static_cast<unsigned>(k.w[shift >> 6] >> (shift & 63)) & 0xffu;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kSortThreads) radix_hist(const uint64_t* __restrict__ keys, long long m,
+                                                           int shift, unsigned* __restrict__ counts,
+                                                           long long ntiles) {
+  __shared__ unsigned s_hist[kSortWarps][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const long long tile = blockIdx.x;
+  const long long base = tile * kSortTile + static_cast<long long>(warp) * kWarpSlice;
+#pragma unroll 4
+  for (int j = 0; j < kSortItems; ++j) {
+    const long long i = base + j * 32 + lane;
+    if (i < m) {
+      const Key<W> k = load_key<W>(keys, i);
+      atomicAdd(&s_hist[warp][digit_of<W>(k, shift)], 1u);
+    }
+  }
+  __syncthreads();
+  const int d = threadIdx.x;  // 256 threads = 256 digits
+  unsigned sum = 0;
+#pragma unroll
+  for (int w = 0; w < kSortWarps; ++w) sum += s_hist[w][d];
+  counts[static_cast<long long>(d) * ntiles + tile] = sum;
+}
+
+// --- exclusive scan of unsigned counters (3 phases) -----------------------
+
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* s_tmp, unsigned* total) {
+  // s_tmp: >= 32 entries
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    unsigned w = lane < nw ? s_tmp[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) s_tmp[lane] = w;
+  }
+  __syncthreads();
+  const unsigned warp_prefix = warp > 0 ? s_tmp[warp - 1] : 0u;
+  if (total) *total = s_tmp[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return warp_prefix + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce(const unsigned* __restrict__ in, long long n,
+                                                            unsigned* __restrict__ partial) {
+  __shared__ unsigned s_tmp[32];
+  const long long base = static_cast<long long>(blockIdx.x) * kScanChunk;
+  unsigned sum = 0;
+  for (int j = 0; j < kScanItems; ++j) {
+    const long long i = base + static_cast<long long>(j) * kScanThreads + threadIdx.x;
+    if (i < n) sum += in[i];
+  }
+  unsigned total;
+  block_exclusive_scan(sum, s_tmp, &total);
+  if (threadIdx.x == 0) partial[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) scan_partials(unsigned* __restrict__ partial, long long n) {
+  __shared__ unsigned s_tmp[32];
+  unsigned carry = 0;
+  for (long long base = 0; base < n; base += blockDim.x) {
+    const long long i = base + threadIdx.x;
+    const unsigned v = i < n ? partial[i] : 0u;
+    unsigned total;
+    const unsigned ex = block_exclusive_scan(v, s_tmp, &total);
+    if (i < n) partial[i] = carry + ex;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_down(unsigned* __restrict__ data, long long n,
+                                                          const unsigned* __restrict__ partial) {
+  __shared__ unsigned s_tmp[32];
+  const long long base = static_cast<long long>(blockIdx.x) * kScanChunk;
+  // thread t owns kScanItems consecutive counters (blocked arrangement)
+  const long long first = base + static_cast<long long>(threadIdx.x) * kScanItems;
+  unsigned v[kScanItems];
+  unsigned sum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    v[j] = (first + j < n) ? data[first + j] : 0u;
+    sum += v[j];
+  }
+  unsigned run = block_exclusive_scan(sum, s_tmp, nullptr) + partial[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    if (first + j < n) data[first + j] = run;
+    run += v[j];
+  }
+}
+
+// --- stable scatter ------------------------------------------------------------
+
+template <int W, int P>
+__global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __restrict__ keys_in,
+                                                              const void* __restrict__ pay_in,
+                                                              uint64_t* __restrict__ keys_out,
+                                                              void* __restrict__ pay_out, long long m, int shift,
+                                                              const unsigned* __restrict__ offsets,
+                                                              long long ntiles) {
+  __shared__ unsigned s_warp[kSortWarps][256];
+  __shared__ unsigned s_base[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&s_warp[0][0])[i] = 0;
+  const long long tile = blockIdx.x;
+  s_base[threadIdx.x] = offsets[static_cast<long long>(threadIdx.x) * ntiles + tile];
+  __syncthreads();
+
+  const long long base = tile * kSortTile + static_cast<long long>(warp) * kWarpSlice;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  Key<W> k[kSortItems];
+  uint64_t pv[kSortItems];
+  unsigned rank[kSortItems];
+  unsigned dig[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const long long i = base + j * 32 + lane;
+    const bool valid = i < m;
+    if (valid) {
+      k[j] = load_key<W>(keys_in, i);
+      if constexpr (P == 4) pv[j] = static_cast<const unsigned*>(pay_in)[i];
+      if constexpr (P == 8) pv[j] = static_cast<const uint64_t*>(pay_in)[i];
+    }
+    const unsigned d = valid ? digit_of<W>(k[j], shift) : 0x100u + lane;  // invalid lanes: singleton groups
+    dig[j] = d;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned r = __popc(peers & lt_mask);
+    unsigned prior = 0;
+    if (valid) prior = s_warp[warp][d];
+    __syncwarp();
+    if (valid && r == 0) s_warp[warp][d] = prior + __popc(peers);
+    __syncwarp();
+    rank[j] = prior + r;
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;
+    unsigned run = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      const unsigned c = s_warp[w][d];
+      s_warp[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const long long i = base + j * 32 + lane;
+    if (i < m) {
+      const unsigned d = dig[j];
+      const long long dst = static_cast<long long>(s_base[d]) + s_warp[warp][d] + rank[j];
+      store_key<W>(keys_out, dst, k[j]);
+      if constexpr (P == 4) static_cast<unsigned*>(pay_out)[dst] = static_cast<unsigned>(pv[j]);
+      if constexpr (P == 8) static_cast<uint64_t*>(pay_out)[dst] = pv[j];
+    }
+  }
+}
+
+// --- K3 duplicates -----------------------------------------------------------
+
+template <int W>
+__global__ void find_dup_kernel(const uint64_t* __restrict__ keys, long long m, long long* __restrict__ first) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = 1 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m; i += stride) {
+    const Key<W> a = load_key<W>(keys, i - 1);
+    const Key<W> b = load_key<W>(keys, i);
+    bool eq = true;
+#pragma unroll
+    for (int w = 0; w < W; ++w) eq &= (a.w[w] == b.w[w]);
+    if (eq) atomicMin(reinterpret_cast<unsigned long long*>(first), static_cast<unsigned long long>(i));
+  }
+}
+__global__ void dup_init(long long* p) { *p = LLONG_MAX; }
+__global__ void dup_fini(long long* p) {
+  if (*p == LLONG_MAX) *p = -1;
+}
+
+struct SortWs {
+  uint64_t* keys_alt;
+  void* pay_alt;
+  unsigned* counts;
+  unsigned* partial;
+  size_t bytes;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static SortWs carve(void* base, long long m, int W, int P) {
+  SortWs w{};
+  const long long ntiles = (m + kSortTile - 1) / kSortTile;
+  const long long ncounts = 256 * ntiles;
+  const long long nparts = (ncounts + kScanChunk - 1) / kScanChunk;
+  size_t off = 0;
+  char* b = static_cast<char*>(base);
+  w.keys_alt = reinterpret_cast<uint64_t*>(b ? b + off : nullptr);
+  off += align256(static_cast<size_t>(m) * W * 8);
+  w.pay_alt = b ? b + off : nullptr;
+  off += align256(static_cast<size_t>(m) * P);
+  w.counts = reinterpret_cast<unsigned*>(b ? b + off : nullptr);
+  off += align256(static_cast<size_t>(ncounts) * 4);
+  w.partial = reinterpret_cast<unsigned*>(b ? b + off : nullptr);
+  off += align256(static_cast<size_t>(nparts + 1) * 4);
+  w.bytes = off;
+  return w;
+}
+
+template <int W, int P>
+static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, const SortWs& ws, cudaStream_t s) {
+  const long long ntiles = (m + kSortTile - 1) / kSortTile;
+  const long long ncounts = 256 * ntiles;
+  const long long nparts = (ncounts + kScanChunk - 1) / kScanChunk;
+  const int passes = (total_bits + 7) / 8;
+  uint64_t* kin = keys;
+  uint64_t* kout = ws.keys_alt;
+  void* pin = pay;
+  void* pout = ws.pay_alt;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    radix_hist<W><<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, m, shift, ws.counts, ntiles);
+    scan_reduce<<<static_cast<unsigned>(nparts), kScanThreads, 0, s>>>(ws.counts, ncounts, ws.partial);
+    scan_partials<<<1, 1024, 0, s>>>(ws.partial, nparts);
+    scan_down<<<static_cast<unsigned>(nparts), kScanThreads, 0, s>>>(ws.counts, ncounts, ws.partial);
+    radix_scatter<W, P><<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, pin, kout, pout, m, shift,
+                                                                              ws.counts, ntiles);
+    std::swap(kin, kout);
+    std::swap(pin, pout);
+  }
+  ALTO_LAUNCH_CHECK("alto_sort_pairs");
+  if (kin != keys) {
+    ALTO_CUDA_TRY(cudaMemcpyAsync(keys, kin, static_cast<size_t>(m) * W * 8, cudaMemcpyDeviceToDevice, s));
+    if (P > 0)
+      ALTO_CUDA_TRY(cudaMemcpyAsync(pay, pin, static_cast<size_t>(m) * P, cudaMemcpyDeviceToDevice, s));
+  }
+  return ALTO_OK;
+}
+
+}  // namespace alto
+
+using namespace alto;
+
+extern "C" {
+
+size_t alto_sort_workspace_bytes(int64_t m, int32_t n_words, int32_t payload_bytes) {
+  if (m < 0) m = 0;
+  return carve(nullptr, m, n_words, payload_bytes).bytes;
+}
+
+int alto_sort_pairs(uint64_t* keys, void* payload, int64_t m, int32_t n_words, int32_t payload_bytes,
+                    int32_t total_bits, void* workspace, size_t workspace_bytes, void* stream) {
+  ALTO_REQUIRE(n_words == 1 || n_words == 2, "n_words must be 1 or 2");
+  ALTO_REQUIRE(payload_bytes == 0 || payload_bytes == 4 || payload_bytes == 8, "payload_bytes must be 0, 4 or 8");
+  ALTO_REQUIRE(total_bits >= 0 && total_bits <= 64 * n_words, "total_bits out of range");
+  ALTO_REQUIRE(m >= 0 && m < (1ll << 32) - 1, "sort supports fewer than 2^32 elements");
+  if (m <= 1 || total_bits == 0) return ALTO_OK;
+  const SortWs ws = carve(workspace, m, n_words, payload_bytes);
+  ALTO_REQUIRE(workspace != nullptr && workspace_bytes >= ws.bytes, "sort workspace too small");
+  cudaStream_t s = as_stream(stream);
+  if (n_words == 1) {
+    if (payload_bytes == 0) return sort_impl<1, 0>(keys, payload, m, total_bits, ws, s);
+    if (payload_bytes == 4) return sort_impl<1, 4>(keys, payload, m, total_bits, ws, s);
+    return sort_impl<1, 8>(keys, payload, m, total_bits, ws, s);
+  }
+  if (payload_bytes == 0) return sort_impl<2, 0>(keys, payload, m, total_bits, ws, s);
+  if (payload_bytes == 4) return sort_impl<2, 4>(keys, payload, m, total_bits, ws, s);
+  return sort_impl<2, 8>(keys, payload, m, total_bits, ws, s);
+}
+
+int alto_find_duplicate(const uint64_t* keys, int64_t m, int32_t n_words, int64_t* d_first, void* stream) {
+  ALTO_REQUIRE(n_words == 1 || n_words == 2, "n_words must be 1 or 2");
+  cudaStream_t s = as_stream(stream);
+  auto* f = reinterpret_cast<long long*>(d_first);
+  dup_init<<<1, 1, 0, s>>>(f);
+  if (m > 1) {
+    const int grid = grid_for(m, 256);
+    if (n_words == 1)
+      find_dup_kernel<1><<<grid, 256, 0, s>>>(keys, m, f);
+    else
+      find_dup_kernel<2><<<grid, 256, 0, s>>>(keys, m, f);
+  }
+  dup_fini<<<1, 1, 0, s>>>(f);
+  ALTO_LAUNCH_CHECK("alto_find_duplicate");
+  return ALTO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,244 @@
+"""MTTKRP on the B200: drop-in for pkg/src/altotensor/mttkrp.py.
+
+Engines (all device code in libalto_b200.so):
+  * streaming tile kernel (`mttkrp_stream`, alto_mttkrp) — the fast path:
+    per-CTA interval buffers in shared memory with a float64 merge, or
+    float64 atomics for wide tiles.  Used for Atomic plans (like the
+    reference's atomic path it is not bitwise reproducible across runs).
+  * exact-order engine (`mttkrp_exact`, alto_mttkrp_exact) — deterministic:
+    per-row sums in element order, split at partition boundaries and merged
+    in ascending partition order, in float64.  This is exactly the
+    arithmetic order of mttkrp_seq (mttkrp.py:108-117) and of the Buffered
+    stage + pull (mttkrp.py:148-172), so results are bitwise equal to the
+    reference on float64 inputs and independent of `workers`.
+  * COO kernel (`mttkrp_oracle`) over a coordinate list.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .coo import CooTensor
+from .format import (AltoTensor, ConflictPlan, PartitionSet, Strategy,
+                     apply_boundary_flags, partition, plan_conflicts,
+                     read_flags_device)
+from .layout import c_layout, device_tables
+
+# The reference's host chunk size (mttkrp.py:39); kept for API parity.
+CHUNK = 1 << 17
+# Elements per CTA tile of the streaming kernel.
+DEFAULT_TILE = 1024
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _is_torch(x) -> bool:
+    torch = _torch()
+    return isinstance(x, torch.Tensor)
+
+
+def _check_factors(dims: Sequence[int], factors, mode: int) -> int:
+    """Shape validation with the reference's messages (mttkrp.py:42-61)."""
+    if not 0 <= mode < len(dims):
+        raise ValueError(f"mode {mode} out of range for order {len(dims)}")
+    if len(factors) != len(dims):
+        raise ValueError(f"expected {len(dims)} factor matrices, got {len(factors)}")
+    rank = None
+    for n, f in enumerate(factors):
+        if f.ndim != 2:
+            raise ValueError(f"factor {n} must be 2-D, got {f.ndim}-D")
+        if f.shape[0] != dims[n]:
+            raise ValueError(f"factor {n} has {f.shape[0]} rows, mode extent is {dims[n]}")
+        if rank is None:
+            rank = f.shape[1]
+        elif f.shape[1] != rank:
+            raise ValueError("factor matrices must share one rank")
+    return int(rank)
+
+
+def factors_to_device(factors, dtype=None) -> list:
+    """Factors as contiguous device tensors (float64 unless dtype/torch input says otherwise)."""
+    torch = _torch()
+    dev = _lib.cuda_device()
+    out = []
+    for f in factors:
+        if isinstance(f, torch.Tensor):
+            dt = dtype or (torch.float32 if f.dtype == torch.float32 else torch.float64)
+            out.append(f.to(device=dev, dtype=dt).contiguous())
+        else:
+            a = np.asarray(f)
+            dt = dtype or (torch.float32 if a.dtype == np.float32 else torch.float64)
+            out.append(torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dt).contiguous())
+    return out
+
+
+def _dt_code(t) -> int:
+    torch = _torch()
+    return _lib.ALTO_F32 if t.dtype == torch.float32 else _lib.ALTO_F64
+
+
+def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_out: int = 1):
+    lay = tensor.layout
+    a = _lib.CMttkrpArgs()
+    cl = c_layout(lay)
+    a.lay = ctypes.pointer(cl)
+    a.d_tables = device_tables(lay).data_ptr()
+    a.keys = tensor.keys.data_ptr()
+    a.values = tensor.vals.data_ptr()
+    a.m = tensor.nnz
+    a.mode = mode
+    a.rank = int(fdev[0].shape[1])
+    a.value_dtype = _dt_code(tensor.vals)
+    fdt = {_dt_code(f) for f in fdev}
+    if len(fdt) != 1:
+        raise ValueError("factor matrices must share one dtype")
+    a.factor_dtype = fdt.pop()
+    for n, f in enumerate(fdev):
+        a.factors[n] = f.data_ptr()
+    a.out = out.data_ptr()
+    a.tile = tile
+    a.tile_lo = None
+    a.tile_hi = None
+    a.zero_out = zero_out
+    return a, cl
+
+
+def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int = DEFAULT_TILE,
+                  zero_out: bool = True):
+    """Fast streaming ALTO MTTKRP on device tensors -> (I_mode, R) float64 device tensor."""
+    torch = _torch()
+    rank = int(fdev[0].shape[1])
+    dim = tensor.layout.dims[mode]
+    if out is None:
+        out = torch.empty((dim, rank), dtype=torch.float64, device=tensor.keys.device)
+    a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
+    _lib.check(_lib.load().alto_mttkrp(ctypes.byref(a), _lib.stream_ptr()), "alto_mttkrp")
+    return out
+
+
+def row_index(tensor: AltoTensor, mode: int):
+    """Per-mode (row_perm, row_ptr): elements sorted by (coordinate, position), cached."""
+    torch = _torch()
+    key = ("row_index", mode)
+    hit = tensor._cache.get(key)
+    if hit is not None:
+        return hit
+    lib = _lib.load()
+    lay = tensor.layout
+    m = tensor.nnz
+    dim = lay.dims[mode]
+    dev = tensor.keys.device
+    perm = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    ptr = torch.empty(dim + 1, dtype=torch.int64, device=dev)
+    ws_bytes = lib.alto_row_index_workspace_bytes(m, dim)
+    ws = torch.empty(max(int(ws_bytes), 8), dtype=torch.uint8, device=dev)
+    _lib.check(lib.alto_row_index(c_layout(lay), device_tables(lay).data_ptr(), tensor.keys.data_ptr(), m, mode,
+                                  perm.data_ptr(), ptr.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr()),
+               "alto_row_index")
+    tensor._cache[key] = (perm, ptr)
+    return perm, ptr
+
+
+def mttkrp_exact(tensor: AltoTensor, fdev: list, mode: int, part_offsets=None, out=None):
+    """Deterministic exact-order MTTKRP -> (I_mode, R) float64 device tensor."""
+    torch = _torch()
+    rank = int(fdev[0].shape[1])
+    dim = tensor.layout.dims[mode]
+    dev = tensor.keys.device
+    if out is None:
+        out = torch.empty((dim, rank), dtype=torch.float64, device=dev)
+    if part_offsets is None:
+        part_offsets = np.asarray([0, tensor.nnz], dtype=np.int64)
+    offs = np.asarray(part_offsets, dtype=np.int64)
+    key = ("part_off", offs.tobytes())
+    d_off = tensor._cache.get(key)
+    if d_off is None:
+        d_off = torch.from_numpy(offs.copy()).to(dev)
+        tensor._cache[key] = d_off
+    perm, ptr = row_index(tensor, mode)
+    a, _keep = _args(tensor, fdev, mode, out)
+    _lib.check(_lib.load().alto_mttkrp_exact(ctypes.byref(a), perm.data_ptr(), ptr.data_ptr(), d_off.data_ptr(),
+                                             len(offs) - 1, _lib.stream_ptr()), "alto_mttkrp_exact")
+    return out
+
+
+def _finish(out_dev, like_torch: bool):
+    return out_dev if like_torch else out_dev.cpu().numpy()
+
+
+def mttkrp_oracle(tensor: CooTensor, factors, mode: int):
+    """COO MTTKRP (mttkrp.py:64-77) on the device, float64 atomics."""
+    torch = _torch()
+    rank = _check_factors(tensor.dims, factors, mode)
+    dev = _lib.cuda_device()
+    out = torch.empty((tensor.dims[mode], rank), dtype=torch.float64, device=dev)
+    fdev = factors_to_device(factors, torch.float64)
+    coords = torch.from_numpy(tensor.coords).to(dev)
+    vals = torch.from_numpy(tensor.values).to(dev)
+    arr = (ctypes.c_void_p * len(fdev))(*[f.data_ptr() for f in fdev])
+    _lib.check(_lib.load().alto_mttkrp_coo(coords.data_ptr(), vals.data_ptr(), tensor.nnz, tensor.order, mode, rank,
+                                           arr, out.data_ptr(), tensor.dims[mode], _lib.stream_ptr()),
+               "alto_mttkrp_coo")
+    return _finish(out, any(_is_torch(f) for f in factors))
+
+
+def mttkrp_seq(tensor: AltoTensor, factors, mode: int):
+    """Sequential-order MTTKRP (mttkrp.py:108-117): exact-order engine, one partition."""
+    _check_factors(tensor.layout.dims, factors, mode)
+    fdev = factors_to_device(factors)
+    return _finish(mttkrp_exact(tensor, fdev, mode), any(_is_torch(f) for f in factors))
+
+
+def _any_flag(tensor: AltoTensor, flag_bit: int) -> bool:
+    if tensor.nnz == 0:
+        return False
+    return bool(read_flags_device(tensor, flag_bit).any().item())
+
+
+def mttkrp_par(tensor: AltoTensor, parts: PartitionSet, plan: ConflictPlan, factors, mode: int,
+               workers: int = 1):
+    """Plan-driven MTTKRP (mttkrp.py:227-251).
+
+    Buffered plans run the exact-order engine over the plan's partitions
+    (bitwise deterministic, independent of `workers`); Atomic plans run the
+    streaming kernel.  `workers` is validated but has no effect on device.
+    """
+    _check_factors(tensor.layout.dims, factors, mode)
+    if workers < 1:
+        raise ValueError("workers must be at least 1")
+    if plan.mode != mode:
+        raise ValueError(f"plan is for mode {plan.mode}, kernel asked for {mode}")
+    if not np.array_equal(plan.offsets, parts.offsets):
+        raise ValueError("plan and partition set do not match")
+    fdev = factors_to_device(factors)
+    like = any(_is_torch(f) for f in factors)
+    if plan.strategy is Strategy.BUFFERED:
+        return _finish(mttkrp_exact(tensor, fdev, mode, np.asarray(parts.offsets)), like)
+    if plan.flag_bit is not None and plan.overlaps is not None and any(plan.overlaps) and tensor.nnz:
+        if not _any_flag(tensor, plan.flag_bit):
+            raise ValueError("plan expects boundary flags; apply_boundary_flags first")
+    return _finish(mttkrp_stream(tensor, fdev, mode), like)
+
+
+def mttkrp(tensor: AltoTensor, factors, mode: int, workers: int = 1, partitions: int | None = None,
+           strategy: Strategy | None = None):
+    """Partition, plan, flag if needed, and run (mttkrp.py:254-271)."""
+    torch = _torch()
+    rank = _check_factors(tensor.layout.dims, factors, mode)
+    if tensor.nnz == 0:
+        z = np.zeros((tensor.layout.dims[mode], rank), dtype=np.float64)
+        return torch.from_numpy(z).to(_lib.cuda_device()) if any(_is_torch(f) for f in factors) else z
+    count = min(partitions if partitions is not None else workers, tensor.nnz)
+    parts = partition(tensor, max(count, 1))
+    plan = plan_conflicts(tensor, parts, mode, force_strategy=strategy)
+    if plan.strategy is Strategy.ATOMIC and plan.flag_bit is not None:
+        tensor = apply_boundary_flags(tensor, plan)
+    return mttkrp_par(tensor, parts, plan, factors, mode, workers)

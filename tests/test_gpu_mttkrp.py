@@ -1,0 +1,234 @@
+"""Device MTTKRP engines against the reference-produced fixtures and the
+oracle.  The exact-order engine must be BITWISE equal to the reference
+(mttkrp_seq, Buffered mttkrp_par) on float64 data; the streaming kernel
+within 1e-12 (fp64) / 1e-5 (fp32) relative Frobenius error."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES, load_golden, rel_error
+from oracle import alto_oracle as orc
+from paper_2102_10245_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def seeded_factors(dims, rank, seed=0):
+    rng = np.random.default_rng(seed)
+    return [rng.random((d, rank)) for d in dims]
+
+
+def golden_setup(at, name):
+    data, meta = load_golden(name)
+    if "coords" in data:
+        coords, values = data["coords"], data["values"]
+    else:
+        st = synth.make_tensor(1) if name == "cfg1" else synth.make_tensor(2, nnz=200_000)
+        coords, values = st.coords, st.values.astype(np.float64)
+    coo = at.CooTensor(meta["dims"], coords, values)
+    rng = np.random.default_rng(meta["fseed"])
+    factors = [rng.random((d, meta["rank"])) for d in meta["dims"]]
+    return data, meta, coo, factors
+
+
+def compare(data, meta, key, out, tol):
+    if meta.get("project"):
+        u = np.random.default_rng(99).random(meta["rank"])
+        assert rel_error(out @ u, data[key + "_proj"]) <= max(tol, 1e-15), key
+        return
+    if tol == 0:
+        assert np.array_equal(out, data[key]), (key, rel_error(out, data[key]))
+    else:
+        assert rel_error(out, data[key]) <= tol, (key, rel_error(out, data[key]))
+
+
+MTTKRP_CASES = [n for n in GOLDEN_CASES if load_golden(n)[1]["with_mttkrp"]]
+
+
+@pytest.mark.parametrize("name", MTTKRP_CASES)
+def test_engines_match_reference(at, name):
+    data, meta, coo, factors = golden_setup(at, name)
+    alto = at.build_alto(coo)
+    for mode in range(len(meta["dims"])):
+        # exact-order engine == reference mttkrp_seq, bit for bit
+        compare(data, meta, f"m{mode}_seq", at.mttkrp_seq(alto, factors, mode), 0)
+        compare(data, meta, f"m{mode}_oracle", at.mttkrp_oracle(coo, factors, mode), 1e-12)
+        for count in meta["counts"]:
+            parts = at.partition(alto, count)
+            plan = at.plan_conflicts(alto, parts, mode, force_strategy=at.Strategy.BUFFERED)
+            compare(data, meta, f"L{count}_m{mode}_buffered_mttkrp",
+                    at.mttkrp_par(alto, parts, plan, factors, mode, workers=4), 0)
+            plan = at.plan_conflicts(alto, parts, mode, force_strategy=at.Strategy.ATOMIC)
+            run = at.apply_boundary_flags(alto, plan) if plan.flag_bit is not None else alto
+            compare(data, meta, f"L{count}_m{mode}_atomic_mttkrp",
+                    at.mttkrp_par(run, parts, plan, factors, mode, workers=4), 1e-12)
+
+
+class TestParallelSemantics:
+    """pkg/tests/test_mttkrp.py:117-226 on the device."""
+
+    @pytest.fixture
+    def setup(self, at):
+        t = at.random_tensor((25, 30, 18), 2500, seed=10)
+        return t, at.build_alto(t), seeded_factors(t.dims, 8, seed=11)
+
+    def test_buffered_bitwise_deterministic(self, at, setup):
+        _, alto, factors = setup
+        runs = [at.mttkrp(alto, factors, 1, workers=w, partitions=6, strategy=at.Strategy.BUFFERED)
+                for w in (1, 2, 4, 8)]
+        for out in runs[1:]:
+            assert np.array_equal(runs[0], out)
+
+    def test_strategy_equivalence(self, at, setup):
+        t, alto, factors = setup
+        for mode in range(3):
+            ref = orc.mttkrp_coo(t.coords, t.values, factors, mode)
+            outs = [at.mttkrp_seq(alto, factors, mode)]
+            for s in at.Strategy:
+                outs.append(at.mttkrp(alto, factors, mode, workers=4, partitions=8, strategy=s))
+            for a in outs:
+                assert rel_error(a, ref) <= 1e-12
+
+    def test_flag_soundness(self, at, setup):
+        _, alto, factors = setup
+        parts = at.partition(alto, 8)
+        for mode in range(3):
+            plan = at.plan_conflicts(alto, parts, mode, force_strategy=at.Strategy.ATOMIC)
+            out = at.mttkrp_par(at.apply_boundary_flags(alto, plan), parts, plan, factors, mode, workers=4)
+            all_out = at.mttkrp_par(alto, parts, dataclasses.replace(plan, flag_bit=None), factors, mode, 4)
+            assert rel_error(out, all_out) <= 1e-12
+
+    def test_linearity(self, at, setup):
+        _, alto, factors = setup
+        scaled = at.AltoTensor(alto.layout, alto.indices, 3.5 * alto.values)
+        for s in at.Strategy:
+            a = at.mttkrp(scaled, factors, 2, workers=2, partitions=4, strategy=s)
+            b = 3.5 * at.mttkrp(alto, factors, 2, workers=2, partitions=4, strategy=s)
+            assert rel_error(a, b) <= 1e-12
+
+    def test_atomic_requires_flags(self, at, setup):
+        _, alto, factors = setup
+        parts = at.partition(alto, 8)
+        plan = at.plan_conflicts(alto, parts, 0, force_strategy=at.Strategy.ATOMIC)
+        assert any(plan.overlaps)
+        with pytest.raises(ValueError, match="flags"):
+            at.mttkrp_par(alto, parts, plan, factors, 0, workers=2)
+
+    def test_plan_mismatch(self, at, setup):
+        _, alto, factors = setup
+        parts, other = at.partition(alto, 4), at.partition(alto, 5)
+        plan = at.plan_conflicts(alto, parts, 0)
+        with pytest.raises(ValueError, match="mode"):
+            at.mttkrp_par(alto, parts, plan, factors, 1, workers=1)
+        with pytest.raises(ValueError, match="partition"):
+            at.mttkrp_par(alto, other, plan, factors, 0, workers=1)
+        with pytest.raises(ValueError, match="workers"):
+            at.mttkrp_par(alto, parts, plan, factors, 0, workers=0)
+
+    def test_shape_validation(self, at):
+        t = at.random_tensor((4, 4, 4), 10, seed=0)
+        good = seeded_factors(t.dims, 2)
+        with pytest.raises(ValueError, match="mode"):
+            at.mttkrp_oracle(t, good, 3)
+        with pytest.raises(ValueError, match="factor matrices"):
+            at.mttkrp_oracle(t, good[:2], 0)
+        with pytest.raises(ValueError, match="rows"):
+            at.mttkrp_oracle(t, [np.ones((5, 2)), np.ones((4, 2)), np.ones((4, 2))], 0)
+        with pytest.raises(ValueError, match="rank"):
+            at.mttkrp_oracle(t, [np.ones((4, 2)), np.ones((4, 3)), np.ones((4, 2))], 0)
+
+    def test_empty_tensor(self, at):
+        e = at.AltoTensor(at.build_masks((4, 8, 2)), np.empty((0, 1), np.uint64), np.empty(0))
+        assert not at.mttkrp_seq(e, seeded_factors((4, 8, 2), 3), 1).any()
+        out = at.mttkrp(e, seeded_factors((4, 8, 2), 2), 0, workers=4)
+        assert out.shape == (4, 2) and not out.any()
+
+    def test_pipeline_clamping(self, at):
+        t = at.random_tensor((4, 100, 4), 64, seed=14)
+        alto = at.build_alto(t)
+        factors = seeded_factors(t.dims, 2, seed=15)
+        assert rel_error(at.mttkrp(alto, factors, 1, workers=2, partitions=1000),
+                         orc.mttkrp_coo(t.coords, t.values, factors, 1)) <= 1e-12
+
+    def test_order_one_and_two(self, at):
+        t1 = at.CooTensor((10,), [[1], [4], [7]], [1.0, 2.0, 3.0])
+        a1 = at.build_alto(t1)
+        f = seeded_factors((10,), 3)
+        assert np.array_equal(at.mttkrp_seq(a1, f, 0), orc.mttkrp_seq(orc.build_layout((10,)), a1.indices,
+                                                                       a1.values, f, 0))
+        t2 = at.random_tensor((30, 20), 200, seed=1)
+        a2 = at.build_alto(t2)
+        f2 = seeded_factors((30, 20), 4)
+        for mode in range(2):
+            ref = orc.mttkrp_coo(t2.coords, t2.values, f2, mode)
+            assert rel_error(at.mttkrp(a2, f2, mode, partitions=3, strategy=at.Strategy.ATOMIC), ref) <= 1e-12
+
+
+class TestStreamKernel:
+    """The fast path at fp32 against the fp64 oracle (north-star bar 1e-5)."""
+
+    WIDE = synth.SynthConfig("cfg9", (1 << 22, 1 << 22, 1 << 21), 0, (("zipf", 1.05),) * 3, "uniform01",
+                             "float32", 16)
+
+    @pytest.mark.parametrize("cfg,nnz,rank", [(2, 300_000, 16), (3, 200_000, 32), (4, 300_000, 16),
+                                              ("wide", 300_000, 16), (1, 100_000, 16)])
+    def test_configs_vs_oracle(self, at, cfg, nnz, rank):
+        """fp32 configs at 1e-5 (cfg1: fp64 at 1e-12).  'wide' = 65-bit,
+        128-bit-key layout with the cfg5 Zipf law at materialisable extents."""
+        import torch
+
+        from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
+
+        st = synth.make_tensor(self.WIDE if cfg == "wide" else cfg, nnz=nnz)
+        if cfg == "wide":
+            cfg = 9
+        dims = st.config.dims
+        coo = at.CooTensor(dims, st.coords, st.values.astype(np.float64))
+        fp32 = st.config.value_dtype == "float32"
+        alto = at.build_alto(coo, dtype="float32" if fp32 else "float64")
+        rng = np.random.default_rng(synth.SEED_FACTOR_BASE + cfg)
+        factors = [rng.random((d, rank)).astype(np.float32 if fp32 else np.float64) for d in dims]
+        fdev = factors_to_device(factors)
+        f64 = [f.astype(np.float64) for f in factors]
+        tol = 1e-5 if fp32 else 1e-12
+        for mode in range(len(dims)):
+            ref = orc.mttkrp_coo(st.coords, st.values.astype(np.float64), f64, mode)
+            for tile in (256, 1024, 4096):
+                out = mttkrp_stream(alto, fdev, mode, tile=tile).cpu().numpy()
+                assert rel_error(out, ref) <= tol, (cfg, mode, tile, rel_error(out, ref))
+            torch.cuda.synchronize()
+
+    def test_accumulates_into_out(self, at):
+        from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
+
+        t = at.random_tensor((40, 30, 20), 3000, seed=5)
+        alto = at.build_alto(t)
+        fdev = factors_to_device(seeded_factors(t.dims, 16, 1))
+        a = mttkrp_stream(alto, fdev, 0)
+        b = mttkrp_stream(alto, fdev, 0, out=a.clone(), zero_out=False)
+        assert rel_error(b.cpu().numpy(), 2 * a.cpu().numpy()) <= 1e-15
+
+    def test_large_linearity(self, at):
+        """Size-independent property at 5M elements on the cfg2 law:
+        MTTKRP(2X) == 2 MTTKRP(X) and mode sums are consistent."""
+        import torch
+
+        from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
+
+        st = synth.make_tensor(2, nnz=5_000_000)
+        coo = at.CooTensor(st.config.dims, st.coords, st.values.astype(np.float64))
+        alto = at.build_alto(coo, dtype="float32")
+        ones = [torch.ones((d, 16), dtype=torch.float32, device="cuda") for d in st.config.dims]
+        total = float(alto.vals.double().sum())
+        for mode in range(3):
+            out = mttkrp_stream(alto, ones, mode)
+            # all-ones factors: every column sums to sum(values) (test_mttkrp.py:45-52 idea)
+            col = out.sum(0).cpu().numpy()
+            assert np.allclose(col, total, rtol=1e-6)
+        f = factors_to_device(seeded_factors(st.config.dims, 16, 3), torch.float32)
+        two = at.AltoTensor(alto.layout, alto.keys, alto.vals * 2)
+        a = mttkrp_stream(alto, f, 1)
+        b = mttkrp_stream(two, f, 1)
+        assert rel_error(b.cpu().numpy(), 2 * a.cpu().numpy()) <= 1e-6
