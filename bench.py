@@ -228,7 +228,7 @@ def run_b200(args):
         for mode in range(N):
             if ev is not None:
                 ev[mode][0].record(stream)
-            mttkrp_stream(alto, fdev, mode, out=outs[mode], tile=args.tile)
+            mttkrp_stream(alto, fdev, mode, out=outs[mode], tile=args.tile, hot=not args.no_hot)
             if ev is not None:
                 ev[mode][1].record(stream)
             if ws > 1:
@@ -374,6 +374,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-cpals", action="store_true")
+    ap.add_argument("--no-hot", action="store_true", help="disable the hot-row plan (A/B)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -145,11 +145,27 @@ typedef struct alto_mttkrp_args {
   int32_t factor_dtype;          /* ALTO_F32 / ALTO_F64 */
   const void* factors[ALTO_MAX_ORDER]; /* (I_n, rank) row-major, factor_dtype */
   double* out;                   /* (I_mode, rank) float64, accumulated into */
-  int32_t tile;                  /* elements per tile (plan granularity)   */
-  const int32_t* tile_lo;        /* (ntiles, order) from alto_tile_intervals */
-  const int32_t* tile_hi;
+  int32_t tile;                  /* elements per tile (multiple of 256, <= 1024) */
   int32_t zero_out;              /* 1: out is zeroed first (stream-ordered) */
+  /* Hot-row plan (optional, from alto_hot_plan): rows with many elements
+   * are touched by nearly every tile, and same-address float64 REDs from all
+   * tiles serialise in one L2 slice.  Their per-tile partials go instead to
+   * `hot_copies` replicated buffers (tile % hot_copies), reduced into `out`
+   * by a second kernel in a fixed order.  hot_slot: (I_mode,) int32, slot or
+   * -1; hot_rows: (n_hot,) int32; hot_buf: hot_copies * n_hot * rank float64,
+   * zero on entry and left zero on exit. */
+  const int32_t* hot_slot;
+  const int32_t* hot_rows;
+  int32_t n_hot;
+  int32_t hot_copies;
+  double* hot_buf;
 } alto_mttkrp_args;
+
+/* Build the hot-row plan of one mode from its row pointer (alto_row_index):
+ * rows with more than `tau` elements get slots (at most hmax);
+ * *d_nhot (device int32) receives the slot count. */
+int alto_hot_plan(const int64_t* row_ptr, int64_t dim, int64_t tau, int32_t hmax,
+                  int32_t* hot_slot, int32_t* hot_rows, int32_t* d_nhot, void* stream);
 
 /* K7/K8 — streaming ALTO MTTKRP (mttkrp.py:80-105 contributions,
  * :132-224 conflict resolution).  Each CTA owns a tile of the sorted stream;

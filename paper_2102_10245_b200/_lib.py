@@ -47,9 +47,12 @@ class CMttkrpArgs(Structure):
         ("factors", c_void_p * ALTO_MAX_ORDER),
         ("out", c_void_p),
         ("tile", c_int32),
-        ("tile_lo", c_void_p),
-        ("tile_hi", c_void_p),
         ("zero_out", c_int32),
+        ("hot_slot", c_void_p),
+        ("hot_rows", c_void_p),
+        ("n_hot", c_int32),
+        ("hot_copies", c_int32),
+        ("hot_buf", c_void_p),
     ]
 
 
@@ -75,6 +78,7 @@ SIGNATURES = [
     ("alto_tile_intervals", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                       c_void_p]),
     ("alto_mttkrp", c_int32, [POINTER(CMttkrpArgs), c_void_p]),
+    ("alto_hot_plan", c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("alto_row_index_workspace_bytes", c_size_t, [c_int64, c_int64]),
     ("alto_row_index", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                  c_void_p, c_size_t, c_void_p]),

@@ -201,10 +201,11 @@ class DeviceBackend:
         order = tensor.layout.order
         self.engine = ["exact"] * order
         self.offsets = [None] * order
-        if backend == "oracle":
-            self.engine = ["coo"] * order
-            return
-        if backend == "seq":
+        if backend in ("seq", "oracle"):
+            # The reference's oracle backend delinearizes the ALTO tensor in
+            # stored order and runs np.add.at in that order (cpd.py:159-162),
+            # i.e. the same arithmetic order as mttkrp_seq: the exact-order
+            # engine reproduces both (deterministically).
             return
         force = {"auto": None, "buffered": Strategy.BUFFERED, "atomic": Strategy.ATOMIC}[backend]
         count = max(min(partitions if partitions is not None else workers, tensor.nnz), 1)

@@ -105,14 +105,48 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
         a.factors[n] = f.data_ptr()
     a.out = out.data_ptr()
     a.tile = tile
-    a.tile_lo = None
-    a.tile_hi = None
     a.zero_out = zero_out
+    a.n_hot = 0
     return a, cl
 
 
+# Hot-row plan: rows holding more than HOT_TAU elements appear in almost every
+# tile; their tile partials go to HOT_COPIES replicated buffers instead of
+# contending on one L2 line (see alto_mttkrp_args in include/alto_b200.h).
+HOT_TAU = 1024
+HOT_MAX = 8192
+HOT_COPIES = 32
+
+
+def hot_plan(tensor: AltoTensor, mode: int, rank: int):
+    """Per-(mode, rank) hot-row plan, built once from the row index and cached."""
+    torch = _torch()
+    key = ("hot", mode, rank)
+    if key in tensor._cache:
+        return tensor._cache[key]
+    lib = _lib.load()
+    dim = tensor.layout.dims[mode]
+    dev = tensor.keys.device
+    if tensor.nnz <= HOT_TAU:
+        tensor._cache[key] = None
+        return None
+    _perm, ptr = row_index(tensor, mode)
+    slot = torch.empty(dim, dtype=torch.int32, device=dev)
+    rows = torch.empty(HOT_MAX, dtype=torch.int32, device=dev)
+    nhot = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(lib.alto_hot_plan(ptr.data_ptr(), dim, HOT_TAU, HOT_MAX, slot.data_ptr(), rows.data_ptr(),
+                                 nhot.data_ptr(), _lib.stream_ptr()), "alto_hot_plan")
+    n = int(nhot.item())
+    plan = None
+    if n > 0:
+        buf = torch.zeros(HOT_COPIES * n * rank, dtype=torch.float64, device=dev)
+        plan = (slot, rows, n, HOT_COPIES, buf)
+    tensor._cache[key] = plan
+    return plan
+
+
 def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int = DEFAULT_TILE,
-                  zero_out: bool = True):
+                  zero_out: bool = True, hot: bool = True):
     """Fast streaming ALTO MTTKRP on device tensors -> (I_mode, R) float64 device tensor."""
     torch = _torch()
     rank = int(fdev[0].shape[1])
@@ -120,6 +154,11 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
     if out is None:
         out = torch.empty((dim, rank), dtype=torch.float64, device=tensor.keys.device)
     a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
+    hp = hot_plan(tensor, mode, rank) if hot else None
+    if hp is not None:
+        slot, rows, n, copies, buf = hp
+        a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf = (slot.data_ptr(), rows.data_ptr(), n, copies,
+                                                                   buf.data_ptr())
     _lib.check(_lib.load().alto_mttkrp(ctypes.byref(a), _lib.stream_ptr()), "alto_mttkrp")
     return out
 
