@@ -219,7 +219,8 @@ def run_b200(args):
     rng = np.random.default_rng(synth.SEED_FACTOR_BASE + args.config)
     factors_host = [rng.random((d, R)).astype(fdt) for d in dims]
     fdev = factors_to_device(factors_host)
-    outs = [torch.empty((d, R), dtype=torch.float64, device=dev) for d in dims]
+    odt = torch.float32 if args.out == "f32" else torch.float64
+    outs = [torch.empty((d, R), dtype=odt, device=dev) for d in dims]
     l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     N = len(dims)
@@ -341,6 +342,7 @@ def run_b200(args):
             "config": {"workload": f"{cfg.name}: {'x'.join(map(str, dims))}, {nnz_total} nnz, Zipf(1.1) all modes, "
                                    f"fp32 values, rank {R}; step = MTTKRP all {N} modes",
                        "nnz": nnz_total, "rank": R, "tile": args.tile, "key_bits": lay.total_bits,
+                       "out_dtype": args.out, "hot_plan": not args.no_hot,
                        "l2": "flushed (256 MB write) before every timed step; keys+values "
                              f"{M * (kb + vb) / 1e6:.0f} MB > 126 MB L2",
                        "parallelism": f"key-range shards x{ws}" if ws > 1 else "1 GPU"},
@@ -375,6 +377,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-cpals", action="store_true")
     ap.add_argument("--no-hot", action="store_true", help="disable the hot-row plan (A/B)")
+    ap.add_argument("--out", default="f32", choices=["f32", "f64"], help="MTTKRP output dtype of the bench step")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -144,7 +144,9 @@ typedef struct alto_mttkrp_args {
   int32_t value_dtype;           /* ALTO_F32 / ALTO_F64 */
   int32_t factor_dtype;          /* ALTO_F32 / ALTO_F64 */
   const void* factors[ALTO_MAX_ORDER]; /* (I_n, rank) row-major, factor_dtype */
-  double* out;                   /* (I_mode, rank) float64, accumulated into */
+  void* out;                     /* (I_mode, rank) row-major, out_dtype     */
+  int32_t out_dtype;             /* ALTO_F64 (reference dtype) or ALTO_F32
+                                    (streaming kernel only)                 */
   int32_t tile;                  /* elements per tile (multiple of 256, <= 1024) */
   int32_t zero_out;              /* 1: out is zeroed first (stream-ordered) */
   /* Hot-row plan (optional, from alto_hot_plan): rows with many elements
@@ -168,11 +170,14 @@ int alto_hot_plan(const int64_t* row_ptr, int64_t dim, int64_t tau, int32_t hmax
                   int32_t* hot_slot, int32_t* hot_rows, int32_t* d_nhot, void* stream);
 
 /* K7/K8 — streaming ALTO MTTKRP (mttkrp.py:80-105 contributions,
- * :132-224 conflict resolution).  Each CTA owns a tile of the sorted stream;
- * tiles whose output-mode interval fits on chip accumulate in shared memory
- * and push one fp64 update per touched row (per-tile interval buffer + merge,
- * the Buffered scheme); wider tiles push fp64 atomics per element (Atomic
- * scheme).  Output is float64 like the reference (mttkrp.py:144, :202). */
+ * :132-224 conflict resolution).  Each CTA streams tiles of the sorted
+ * stream; a tile whose output-mode interval is short is counting-sorted by
+ * output row on chip (its interval buffer), its contributions reduced in
+ * registers per row segment and merged with one atomic update per (tile,
+ * row) — the Buffered scheme at CTA granularity; a wide tile merges per
+ * element run (the Atomic scheme).  Hot rows use the replicated buffers of
+ * the hot plan.  Not bitwise reproducible (atomics), like the reference's
+ * atomic path with several workers. */
 int alto_mttkrp(const alto_mttkrp_args* a, void* stream);
 
 /* Exact-order engine (deterministic; bitwise equal to the reference for

@@ -46,6 +46,7 @@ class CMttkrpArgs(Structure):
         ("factor_dtype", c_int32),
         ("factors", c_void_p * ALTO_MAX_ORDER),
         ("out", c_void_p),
+        ("out_dtype", c_int32),
         ("tile", c_int32),
         ("zero_out", c_int32),
         ("hot_slot", c_void_p),

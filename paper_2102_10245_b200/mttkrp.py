@@ -104,6 +104,7 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
     for n, f in enumerate(fdev):
         a.factors[n] = f.data_ptr()
     a.out = out.data_ptr()
+    a.out_dtype = _dt_code(out)
     a.tile = tile
     a.zero_out = zero_out
     a.n_hot = 0
@@ -146,13 +147,16 @@ def hot_plan(tensor: AltoTensor, mode: int, rank: int):
 
 
 def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int = DEFAULT_TILE,
-                  zero_out: bool = True, hot: bool = True):
-    """Fast streaming ALTO MTTKRP on device tensors -> (I_mode, R) float64 device tensor."""
+                  zero_out: bool = True, hot: bool = True, out_dtype=None):
+    """Fast streaming ALTO MTTKRP on device tensors -> (I_mode, R) device tensor
+    (float64 by default; float32 when requested for float32 data/factors)."""
     torch = _torch()
     rank = int(fdev[0].shape[1])
     dim = tensor.layout.dims[mode]
+    if tensor.vals.dtype == torch.float64 and fdev[0].dtype == torch.float32:
+        fdev = [f.double() for f in fdev]  # exact upcast; the kernel pairs f64 values with f64 factors
     if out is None:
-        out = torch.empty((dim, rank), dtype=torch.float64, device=tensor.keys.device)
+        out = torch.empty((dim, rank), dtype=out_dtype or torch.float64, device=tensor.keys.device)
     a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
     hp = hot_plan(tensor, mode, rank) if hot else None
     if hp is not None:

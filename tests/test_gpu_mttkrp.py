@@ -200,6 +200,28 @@ class TestStreamKernel:
                 assert rel_error(out, ref) <= tol, (cfg, mode, tile, rel_error(out, ref))
             torch.cuda.synchronize()
 
+    @pytest.mark.parametrize("cfg,nnz,rank", [(2, 400_000, 16), (3, 150_000, 32), (4, 300_000, 16)])
+    def test_float32_output(self, at, cfg, nnz, rank):
+        """float32 output (RED.F32x4 merge, hot rows in float64) vs the fp64 oracle at 1e-5."""
+        import torch
+
+        from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
+
+        st = synth.make_tensor(cfg, nnz=nnz)
+        dims = st.config.dims
+        alto = at.build_alto(at.CooTensor(dims, st.coords, st.values.astype(np.float64)), dtype="float32")
+        rng = np.random.default_rng(7)
+        factors = [rng.random((d, rank)).astype(np.float32) for d in dims]
+        fdev = factors_to_device(factors)
+        for mode in range(len(dims)):
+            ref = orc.mttkrp_coo(st.coords, st.values.astype(np.float64), [f.astype(np.float64) for f in factors],
+                                 mode)
+            out = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32)
+            assert out.dtype == torch.float32
+            assert rel_error(out.double().cpu().numpy(), ref) <= 1e-5
+            nohot = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, hot=False)
+            assert rel_error(nohot.double().cpu().numpy(), ref) <= 1e-5
+
     def test_accumulates_into_out(self, at):
         from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
 
