@@ -92,6 +92,19 @@ __device__ __forceinline__ Key<W> load_key(const uint64_t* __restrict__ keys, lo
 }
 
 template <int W>
+__device__ __forceinline__ Key<W> load_key_smem(const uint64_t* keys, int i) {
+  Key<W> k;
+  if constexpr (W == 1) {
+    k.w[0] = keys[i];
+  } else {
+    const ulonglong2 v = reinterpret_cast<const ulonglong2*>(keys)[i];
+    k.w[0] = v.x;
+    k.w[1] = v.y;
+  }
+  return k;
+}
+
+template <int W>
 __device__ __forceinline__ void store_key(uint64_t* keys, long long i, const Key<W>& k) {
   if constexpr (W == 1) {
     keys[i] = k.w[0];
