@@ -41,6 +41,7 @@ constexpr int kTileThreads = 256;
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kSortBins = 2048;
 constexpr int kEPT = 4;  // elements per thread in phase A -> tile <= 1024
+constexpr int kRecPad = 4 * kTileThreads;  // words of swizzle headroom (4 per phase-B chunk)
 
 struct StreamParams {
   const uint64_t* keys;
@@ -170,7 +171,7 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
   uint64_t* s_dec = reinterpret_cast<uint64_t*>(smem);
   size_t off = (static_cast<size_t>(L.dec_bytes) * 256 * W * 8 + 15) & ~size_t(15);
   unsigned* s_rec = reinterpret_cast<unsigned*>(smem + off);  // [T][NW]
-  off += static_cast<size_t>(T) * NW * 4;
+  off += static_cast<size_t>(T) * NW * 4 + kRecPad * 4;
   int* s_bin = reinterpret_cast<int*>(smem + off);            // [kSortBins + kTileWarps]
   off += (kSortBins + kTileWarps) * sizeof(int);
   off = (off + 15) & ~size_t(15);
@@ -185,6 +186,11 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
   const int grp = tid / G;
   const int gl = tid % G;
   const int r_lane = 4 * gl;
+  // Record swizzle: phase-B groups read chunks of T/NGROUPS consecutive
+  // records; shifting chunk c by 16*c bytes puts the 8 groups of a warp on
+  // distinct banks (unswizzled, equal strides make it an 8-way conflict).
+  const int chunk_shift = 31 - __clz(max(T / NGROUPS, 1));
+  auto rec_addr = [&](int j) { return j * NW + (j >> chunk_shift) * 4; };
   const unsigned qmask = (G >= 4) ? (0xFu << (lane & ~3)) : 0xffffffffu;
   // input-mode factor bases in record order (mode skipped)
   const F* __restrict__ fin[NIN > 0 ? NIN : 1];
@@ -327,7 +333,7 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
           const int slot = atomicAdd(&s_bin[myrow[k] - lo], 1);
 #pragma unroll
           for (int q = 0; q < NW; q += 4)
-            *reinterpret_cast<uint4*>(s_rec + slot * NW + q) =
+            *reinterpret_cast<uint4*>(s_rec + rec_addr(slot) + q) =
                 make_uint4(rec[k][q], rec[k][q + 1], rec[k][q + 2], rec[k][q + 3]);
         }
     } else {
@@ -337,7 +343,7 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
           const int e = tid + k * kTileThreads;
 #pragma unroll
           for (int q = 0; q < NW; q += 4)
-            *reinterpret_cast<uint4*>(s_rec + e * NW + q) =
+            *reinterpret_cast<uint4*>(s_rec + rec_addr(e) + q) =
                 make_uint4(rec[k][q], rec[k][q + 1], rec[k][q + 2], rec[k][q + 3]);
         }
     }
@@ -381,7 +387,7 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
             unsigned cw[NW];
 #pragma unroll
             for (int q = 0; q < NW; q += 4) {
-              const uint4 t = *reinterpret_cast<const uint4*>(s_rec + j * NW + q);
+              const uint4 t = *reinterpret_cast<const uint4*>(s_rec + rec_addr(j) + q);
               cw[q] = t.x; cw[q + 1] = t.y; cw[q + 2] = t.z; cw[q + 3] = t.w;
             }
             tg[u] = static_cast<int>(cw[RL::TGT]);
@@ -473,7 +479,7 @@ int launch(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaS
   constexpr int NW = RecLayout<NMAX, V>::NW;
   const size_t stage_bytes = (static_cast<size_t>(P.tile) * (W * 8 + sizeof(V)) + 15) & ~size_t(15);
   const size_t smem = ((static_cast<size_t>(d.dec_bytes) * 256 * W * 8 + 15) & ~size_t(15)) +
-                      static_cast<size_t>(P.tile) * NW * 4 +
+                      static_cast<size_t>(P.tile) * NW * 4 + kRecPad * 4 +
                       (((kSortBins + kTileWarps) * sizeof(int) + 15) & ~size_t(15)) + 2 * stage_bytes;
   auto kern = stream_kernel<W, V, F, O, NT, G, VEC, FULLR>;
   if (prep(kern, smem)) return ALTO_ECUDA;
