@@ -161,7 +161,12 @@ typedef struct alto_mttkrp_args {
   int32_t n_hot;
   int32_t hot_copies;
   double* hot_buf;
+  int32_t flags;                 /* ALTO_STREAM_* tuning switches (0 = default) */
 } alto_mttkrp_args;
+
+/* Streaming-kernel tuning switches (alto_mttkrp_args.flags). */
+#define ALTO_STREAM_WARP_AGG 1   /* warp-aggregate in-tile sort atomics */
+#define ALTO_STREAM_FULL_BINS 2  /* scan all sort bins instead of the tile span */
 
 /* Build the hot-row plan of one mode from its row pointer (alto_row_index):
  * rows with more than `tau` elements get slots (at most hmax);

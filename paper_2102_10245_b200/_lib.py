@@ -54,6 +54,7 @@ class CMttkrpArgs(Structure):
         ("n_hot", c_int32),
         ("hot_copies", c_int32),
         ("hot_buf", c_void_p),
+        ("flags", c_int32),
     ]
 
 

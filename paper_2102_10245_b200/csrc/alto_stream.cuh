@@ -57,6 +57,7 @@ struct StreamParams {
   const int* hot_slot;
   int hot_copies;
   double* hot_buf;
+  int flags;  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
 };
 
 template <typename V, typename F>
@@ -290,25 +291,39 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
     if (lane == 0) { s_lo[warp] = lo; s_hi[warp] = hi; }
-    for (int i = tid; i < kSortBins; i += kTileThreads) s_bin[i] = 0;
     __syncthreads();
     lo = s_lo[0]; hi = s_hi[0];
 #pragma unroll
     for (int w = 1; w < kTileWarps; ++w) { lo = min(lo, s_lo[w]); hi = max(hi, s_hi[w]); }
+    const int span = hi - lo + 1;
     // ---- in-tile counting sort by output row ----------------------------
-    if (hi - lo + 1 <= kSortBins) {
-#pragma unroll
-      for (int k = 0; k < kEPT; ++k)
-        if (myrow[k] >= 0) atomicAdd(&s_bin[myrow[k] - lo], 1);
+    // Only the tile's span of bins is touched; equal bins inside a warp are
+    // aggregated with __match_any_sync so hot rows cost one atomic per warp.
+    if (span <= kSortBins) {
+      const bool aggregate = (P.flags & ALTO_STREAM_WARP_AGG) != 0;
+      const int nbins = (P.flags & ALTO_STREAM_FULL_BINS) ? kSortBins : span;
+      for (int i = tid; i < nbins; i += kTileThreads) s_bin[i] = 0;
       __syncthreads();
-      constexpr int BPT = kSortBins / kTileThreads;
-      int loc[BPT];
-      int sum = 0;
+      unsigned peers[kEPT];
+      const unsigned lt = (1u << lane) - 1u;
+      if (aggregate) {
 #pragma unroll
-      for (int q = 0; q < BPT; ++q) {
-        loc[q] = s_bin[tid * BPT + q];
-        sum += loc[q];
+        for (int k = 0; k < kEPT; ++k) {
+          const bool ok = myrow[k] >= 0;
+          const int bin = ok ? myrow[k] - lo : (1 << 30) + lane;
+          peers[k] = __match_any_sync(0xffffffffu, bin);
+          if (ok && (peers[k] & lt) == 0) atomicAdd(&s_bin[bin], __popc(peers[k]));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k)
+          if (myrow[k] >= 0) atomicAdd(&s_bin[myrow[k] - lo], 1);
       }
+      __syncthreads();
+      const int per = (nbins + kTileThreads - 1) / kTileThreads;
+      const int b0 = min(nbins, tid * per), b1 = min(nbins, b0 + per);
+      int sum = 0;
+      for (int i = b0; i < b1; ++i) sum += s_bin[i];
       int x = sum;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -317,25 +332,35 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
       }
       if (lane == 31) s_bin[kSortBins + warp] = x;
       __syncthreads();
-      int wpre = 0;
+      int run = x - sum;
 #pragma unroll
-      for (int w = 0; w < kTileWarps; ++w) wpre += (w < warp) ? s_bin[kSortBins + w] : 0;
-      int run = wpre + x - sum;
-#pragma unroll
-      for (int q = 0; q < BPT; ++q) {
-        s_bin[tid * BPT + q] = run;
-        run += loc[q];
+      for (int w = 0; w < kTileWarps; ++w) run += (w < warp) ? s_bin[kSortBins + w] : 0;
+      for (int i = b0; i < b1; ++i) {
+        const int c = s_bin[i];
+        s_bin[i] = run;
+        run += c;
       }
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < kEPT; ++k)
-        if (myrow[k] >= 0) {
-          const int slot = atomicAdd(&s_bin[myrow[k] - lo], 1);
+      for (int k = 0; k < kEPT; ++k) {
+        const bool ok = myrow[k] >= 0;
+        int slot = 0;
+        if (aggregate) {
+          const int leader = __ffs(peers[k]) - 1;
+          int base = 0;
+          if (ok && leader == lane) base = atomicAdd(&s_bin[myrow[k] - lo], __popc(peers[k]));
+          base = __shfl_sync(0xffffffffu, base, leader);
+          slot = base + __popc(peers[k] & lt);
+        } else if (ok) {
+          slot = atomicAdd(&s_bin[myrow[k] - lo], 1);
+        }
+        if (ok) {
 #pragma unroll
           for (int q = 0; q < NW; q += 4)
             *reinterpret_cast<uint4*>(s_rec + rec_addr(slot) + q) =
                 make_uint4(rec[k][q], rec[k][q + 1], rec[k][q + 2], rec[k][q + 3]);
         }
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < kEPT; ++k)

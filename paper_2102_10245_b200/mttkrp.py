@@ -32,6 +32,8 @@ from .layout import c_layout, device_tables
 CHUNK = 1 << 17
 # Elements per CTA tile of the streaming kernel.
 DEFAULT_TILE = 1024
+# Streaming-kernel tuning switches (ALTO_STREAM_* in include/alto_b200.h).
+STREAM_FLAGS = int(__import__("os").environ.get("ALTO_STREAM_FLAGS", "0"))
 
 
 def _torch():
@@ -108,6 +110,7 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
     a.tile = tile
     a.zero_out = zero_out
     a.n_hot = 0
+    a.flags = STREAM_FLAGS
     return a, cl
 
 
