@@ -168,6 +168,29 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def traffic_from_profile(kernel_tag: str):
+    """Per-launch DRAM bytes (read + write) of the dominant kernel from the
+    latest committed `ncu --set full` capture of this workload (profiles/)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_stream_kernel_ncu.json")))
+    if not files:
+        return None, None
+    try:
+        rows = json.load(open(files[-1]))
+        vals = []
+        for r in rows:
+            if kernel_tag in r["kernel"]:
+                rd = float(r["dram__bytes_read.sum"]["value"])
+                wr = float(r["dram__bytes_write.sum"]["value"])
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                vals.append(rd * scale[r["dram__bytes_read.sum"]["unit"]] +
+                            wr * scale[r["dram__bytes_write.sum"]["unit"]])
+        return (sum(vals) / len(vals) if vals else None), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def flush_l2(buf):
     buf.add_(1.0)
 
@@ -277,6 +300,9 @@ def run_b200(args):
     tot_b = sum(p["bytes_alg"] for p in per_mode)
     tot_t = sum(mode_ms) * 1e-3
     achieved = tot_b / tot_t / 1e9
+    traffic, traffic_src = None, None
+    if ws == 1 and nnz_total == cfg.nnz and args.config == 2 and args.out == "f32" and not args.no_hot:
+        traffic, traffic_src = traffic_from_profile("stream_kernel<1, float, float, float, 3, 4")
 
     # end-to-end through the reference-facing API: mttkrp_par with an Atomic plan
     # (the CLI protocol: prepare once, cli.py:194; per step host factors in,
@@ -348,7 +374,9 @@ def run_b200(args):
                        "parallelism": f"key-range shards x{ws}" if ws > 1 else "1 GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
-                         "traffic": None, "kernel": "mttkrp_tile_kernel", "per_mode": per_mode},
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "bytes_alg_per_launch": tot_b / N, "kernel": "alto::stream_kernel (alto_stream.cuh)",
+                         "per_mode": per_mode},
             "e2e": {"value": N * nnz_total / (e2e_ms * 1e-3), "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "api": "paper_2102_10245_b200.mttkrp_par (Atomic plan) with pinned host fp32 factors in, "
