@@ -8,9 +8,9 @@ Metric: MTTKRP nonzeros/s (mode-averaged: 3*nnz per step / step time).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 N > 1 (torchrun): nonzeros are sharded by linearized-key range (ALTO
-partitions), factors replicated; each step adds an NCCL all-reduce of every
-mode's output (the shared-row exchange at its simplest), timed as the max
-over ranks.
+partitions), factors replicated; each mode's step adds the shared-row
+exchange of dist.py (rows touched by >= 2 shards packed into one NCCL
+all-reduce), timed as the max over ranks.
 """
 
 from __future__ import annotations
@@ -247,6 +247,16 @@ def run_b200(args):
     l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     N = len(dims)
+    xplans = None
+    exch_bytes = 0
+    if ws > 1:
+        # shared-row exchange plan per mode (dist.py): only rows touched by
+        # >= 2 key-range shards cross NVLink, in one all-reduce per mode
+        from paper_2102_10245_b200.dist import DeviceOps, ShardRows, reduce_shared
+
+        xops = DeviceOps(alto, R)
+        xplans = [ShardRows(xops.touched_rows(n)) for n in range(N)]
+        exch_bytes = sum(p.n_shared for p in xplans) * R * (4 if args.out == "f32" else 8)
 
     def step(ev=None):
         for mode in range(N):
@@ -256,7 +266,7 @@ def run_b200(args):
             if ev is not None:
                 ev[mode][1].record(stream)
             if ws > 1:
-                dist.all_reduce(outs[mode])
+                reduce_shared(outs[mode], xplans[mode], xops)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -371,7 +381,8 @@ def run_b200(args):
                        "out_dtype": args.out, "hot_plan": not args.no_hot,
                        "l2": "flushed (256 MB write) before every timed step; keys+values "
                              f"{M * (kb + vb) / 1e6:.0f} MB > 126 MB L2",
-                       "parallelism": f"key-range shards x{ws}" if ws > 1 else "1 GPU"},
+                       "parallelism": f"key-range shards x{ws}" if ws > 1 else "1 GPU",
+                       "exchange_bytes_per_step": exch_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "traffic": traffic, "traffic_source": traffic_src,

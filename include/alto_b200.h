@@ -238,6 +238,29 @@ int alto_fit_terms(const double* mttkrp, const double* f, const double* lambda,
 /* sum of squares of values in float64 (cpd.py:211). */
 int alto_sumsq(const void* values, int32_t dtype, int64_t m, double* out,
                void* ws, size_t ws_bytes, void* stream);
+/* Key-range-sharded CP-ALS pieces (multi-GPU).  row_mask
+ * (I_n bytes, NULL = all rows) selects the rows this shard owns so each row
+ * is counted once before the cross-shard all-reduce. */
+int alto_gram_masked(const void* f, int32_t f_dtype, int64_t rows, int32_t rank, const uint8_t* row_mask,
+                     double* g_partial, void* ws, size_t ws_bytes, void* stream);
+/* X V = M (Cholesky + ridge retry), no normalisation. */
+int alto_solve_rows(const double* v, const double* mttkrp, int64_t rows, int32_t rank, double* x64,
+                    int32_t* d_status, void* ws, size_t ws_bytes, void* stream);
+/* out[r] = sum over masked rows of X[i, r]^2. */
+int alto_colsumsq(const double* x, int64_t rows, int32_t rank, const uint8_t* row_mask, double* out,
+                  void* ws, size_t ws_bytes, void* stream);
+/* lambda = sqrt(colsumsq); X /= lambda (zero-safe); optional float32 copy. */
+int alto_normalize(double* x64, float* x32, int64_t rows, int32_t rank, const double* colsumsq, double* lambda,
+                   const int32_t* d_status, void* stream);
+/* out[0] = sum over masked rows of M[i,r] F[i,r] lambda_r. */
+int alto_fit_inner_masked(const double* mttkrp, const double* f, const double* lambda, int64_t rows, int32_t rank,
+                          const uint8_t* row_mask, double* out, void* ws, size_t ws_bytes, void* stream);
+/* K14 shared-row exchange: buf[i, :] = src[rows[i], :] (pack) and
+ * dst[rows[i], :] = buf[i, :] (unpack); rows (n,) int64 device array. */
+int alto_pack_rows(const void* src, int32_t dtype, const int64_t* rows, int64_t n, int32_t rank, void* buf,
+                   void* stream);
+int alto_unpack_rows(void* dst, int32_t dtype, const int64_t* rows, int64_t n, int32_t rank, const void* buf,
+                     void* stream);
 /* Cast helpers for factor uploads: out32[i] = (float)in64[i]. */
 int alto_cast_f64_f32(const double* in, float* out, int64_t n, void* stream);
 

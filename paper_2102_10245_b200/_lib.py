@@ -96,6 +96,16 @@ SIGNATURES = [
                                  c_size_t, c_void_p]),
     ("alto_sumsq", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_cast_f64_f32", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+    ("alto_pack_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    ("alto_unpack_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    ("alto_gram_masked", c_int32, [c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t,
+                                   c_void_p]),
+    ("alto_solve_rows", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t,
+                                  c_void_p]),
+    ("alto_colsumsq", c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("alto_normalize", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("alto_fit_inner_masked", c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
+                                        c_void_p, c_size_t, c_void_p]),
 ]
 
 _lib = None

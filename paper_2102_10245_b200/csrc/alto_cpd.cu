@@ -179,6 +179,12 @@ __global__ void lambda_kernel(const double* __restrict__ part, int nblocks, int 
   }
 }
 
+__global__ void sqrt_kernel(const double* __restrict__ sumsq, int R, double* __restrict__ lambda,
+                            const int* __restrict__ status) {
+  if (*status == 2) return;
+  for (int c = threadIdx.x; c < R; c += blockDim.x) lambda[c] = sqrt(sumsq[c]);
+}
+
 __global__ void normalize_kernel(double* __restrict__ x64, float* __restrict__ x32, long long rows, int R,
                                  const double* __restrict__ lambda, const int* __restrict__ status) {
   if (*status == 2) return;
@@ -349,6 +355,169 @@ int alto_cast_f64_f32(const double* in, float* out, int64_t n, void* stream) {
   if (n <= 0) return ALTO_OK;
   cast_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(in, out, n);
   ALTO_LAUNCH_CHECK("alto_cast_f64_f32");
+  return ALTO_OK;
+}
+
+}  // extern "C"
+
+// ---- distributed (key-range sharded) CP-ALS pieces --------------------------
+// A shard owns a subset of output rows (rows only it touches, plus shared
+// rows it is the designated owner of); sums over rows (Gram, column norms,
+// fit inner product) take a 0/1 row mask so that every row is counted by
+// exactly one shard before the cross-shard all-reduce.
+
+namespace alto {
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) gram_partial_masked(const T* __restrict__ f, long long rows, int R,
+                                                                   const unsigned char* __restrict__ mask,
+                                                                   double* __restrict__ part) {
+  __shared__ double s_f[32][kMaxRank + 1];
+  const long long chunk = (rows + gridDim.x - 1) / gridDim.x;
+  const long long r0 = blockIdx.x * chunk;
+  const long long r1 = min(rows, r0 + chunk);
+  const int RR = R * R;
+  double acc[(kMaxRank * kMaxRank + kRedThreads - 1) / kRedThreads];
+  const int per = (RR + kRedThreads - 1) / kRedThreads;
+  for (int q = 0; q < per; ++q) acc[q] = 0.0;
+  for (long long base = r0; base < r1; base += 32) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < 32 * R; t += blockDim.x) {
+      const int k = t / R, c = t - k * R;
+      const long long row = base + k;
+      const bool on = row < r1 && (mask == nullptr || mask[row]);
+      s_f[k][c] = on ? static_cast<double>(f[row * R + c]) : 0.0;
+    }
+    __syncthreads();
+    const int nk = static_cast<int>(min(32ll, r1 - base));
+    for (int q = 0; q < per; ++q) {
+      const int idx = threadIdx.x + q * kRedThreads;
+      if (idx < RR) {
+        const int i = idx / R, j = idx - (idx / R) * R;
+        double a = acc[q];
+        for (int k = 0; k < nk; ++k) a = fma(s_f[k][i], s_f[k][j], a);
+        acc[q] = a;
+      }
+    }
+  }
+  for (int q = 0; q < per; ++q) {
+    const int idx = threadIdx.x + q * kRedThreads;
+    if (idx < RR) part[static_cast<long long>(blockIdx.x) * RR + idx] = acc[q];
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) colsumsq_partial(const double* __restrict__ x, long long rows, int R,
+                                                                const unsigned char* __restrict__ mask,
+                                                                double* __restrict__ part) {
+  __shared__ double s_sq[kRedThreads / 32][kMaxRank];
+  const long long chunk = (rows + gridDim.x - 1) / gridDim.x;
+  const long long r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
+  double sq[kMaxRank];
+  for (int c = 0; c < R; ++c) sq[c] = 0.0;
+  for (long long row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
+    if (mask && !mask[row]) continue;
+    for (int c = 0; c < R; ++c) {
+      const double y = x[row * R + c];
+      sq[c] += y * y;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = 0; c < R; ++c) {
+    double s = sq[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) s_sq[warp][c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) s += s_sq[w][threadIdx.x];
+    part[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) inner_partial_masked(const double* __restrict__ mt,
+                                                                    const double* __restrict__ f,
+                                                                    const double* __restrict__ lambda,
+                                                                    long long rows, int R,
+                                                                    const unsigned char* __restrict__ mask,
+                                                                    double* __restrict__ part) {
+  __shared__ double s_tmp[32];
+  const long long n = rows * R;
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  double s = 0.0;
+  for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+    if (mask == nullptr || mask[i / R]) s += (mt[i] * f[i]) * lambda[i % R];
+  s = block_sum_fixed(s, s_tmp);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+}  // namespace alto
+
+extern "C" {
+
+int alto_gram_masked(const void* f, int32_t f_dtype, int64_t rows, int32_t rank, const uint8_t* row_mask,
+                     double* g_partial, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  if (f_dtype == ALTO_F32)
+    gram_partial_masked<float><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const float*>(f), rows, rank,
+                                                                  row_mask, part);
+  else
+    gram_partial_masked<double><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const double*>(f), rows, rank,
+                                                                   row_mask, part);
+  sum_partials<<<1, 256, 0, s>>>(part, kRedBlocks, rank * rank, g_partial);
+  ALTO_LAUNCH_CHECK("alto_gram_masked");
+  return ALTO_OK;
+}
+
+int alto_solve_rows(const double* v, const double* mttkrp, int64_t rows, int32_t rank, double* x64,
+                    int32_t* d_status, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  double* lmat = part + static_cast<size_t>(kRedBlocks) * rank * rank;
+  cholesky_kernel<<<1, 32, 0, s>>>(v, rank, lmat, d_status);
+  solve_rows<<<kRedBlocks, kRedThreads, 0, s>>>(lmat, mttkrp, rows, rank, x64, d_status, part);
+  ALTO_LAUNCH_CHECK("alto_solve_rows");
+  return ALTO_OK;
+}
+
+int alto_colsumsq(const double* x, int64_t rows, int32_t rank, const uint8_t* row_mask, double* out,
+                  void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  colsumsq_partial<<<kRedBlocks, kRedThreads, 0, s>>>(x, rows, rank, row_mask, part);
+  sum_partials<<<1, 64, 0, s>>>(part, kRedBlocks, rank, out);
+  ALTO_LAUNCH_CHECK("alto_colsumsq");
+  return ALTO_OK;
+}
+
+int alto_normalize(double* x64, float* x32, int64_t rows, int32_t rank, const double* colsumsq, double* lambda,
+                   const int32_t* d_status, void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  cudaStream_t s = as_stream(stream);
+  sqrt_kernel<<<1, 64, 0, s>>>(colsumsq, rank, lambda, d_status);
+  normalize_kernel<<<grid_for(rows * rank, 256), 256, 0, s>>>(x64, x32, rows, rank, lambda, d_status);
+  ALTO_LAUNCH_CHECK("alto_normalize");
+  return ALTO_OK;
+}
+
+int alto_fit_inner_masked(const double* mttkrp, const double* f, const double* lambda, int64_t rows, int32_t rank,
+                          const uint8_t* row_mask, double* out, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRank, "rank must be in [1, 64]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  inner_partial_masked<<<kRedBlocks, kRedThreads, 0, s>>>(mttkrp, f, lambda, rows, rank, row_mask, part);
+  sum_scalar<<<1, 32, 0, s>>>(part, kRedBlocks, out);
+  ALTO_LAUNCH_CHECK("alto_fit_inner_masked");
   return ALTO_OK;
 }
 

@@ -125,3 +125,54 @@ int alto_hot_plan(const int64_t* row_ptr, int64_t dim, int64_t tau, int32_t hmax
 }
 
 }  // extern "C"
+
+// ---- K14: shared-row pack/unpack for the multi-GPU exchange -----------------
+namespace alto {
+template <typename T>
+__global__ void pack_rows_kernel(const T* __restrict__ src, const long long* __restrict__ rows, long long n, int R,
+                                 T* __restrict__ dst, int unpack) {
+  const long long total = n * R;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const long long k = i / R;
+    const long long g = rows[k] * R + (i - k * R);
+    if (unpack)
+      const_cast<T*>(src)[g] = dst[i];
+    else
+      dst[i] = src[g];
+  }
+}
+}  // namespace alto
+
+extern "C" {
+int alto_pack_rows(const void* src, int32_t dtype, const int64_t* rows, int64_t n, int32_t rank, void* buf,
+                   void* stream) {
+  if (n <= 0) return ALTO_OK;
+  cudaStream_t s = as_stream(stream);
+  const auto* r = reinterpret_cast<const long long*>(rows);
+  if (dtype == ALTO_F32)
+    pack_rows_kernel<float><<<grid_for(n * rank, 256), 256, 0, s>>>(static_cast<const float*>(src), r, n, rank,
+                                                                     static_cast<float*>(buf), 0);
+  else
+    pack_rows_kernel<double><<<grid_for(n * rank, 256), 256, 0, s>>>(static_cast<const double*>(src), r, n, rank,
+                                                                      static_cast<double*>(buf), 0);
+  ALTO_LAUNCH_CHECK("alto_pack_rows");
+  return ALTO_OK;
+}
+
+int alto_unpack_rows(void* dst, int32_t dtype, const int64_t* rows, int64_t n, int32_t rank, const void* buf,
+                     void* stream) {
+  if (n <= 0) return ALTO_OK;
+  cudaStream_t s = as_stream(stream);
+  const auto* r = reinterpret_cast<const long long*>(rows);
+  if (dtype == ALTO_F32)
+    pack_rows_kernel<float><<<grid_for(n * rank, 256), 256, 0, s>>>(static_cast<const float*>(dst), r, n, rank,
+                                                                     const_cast<float*>(static_cast<const float*>(buf)),
+                                                                     1);
+  else
+    pack_rows_kernel<double><<<grid_for(n * rank, 256), 256, 0, s>>>(
+        static_cast<const double*>(dst), r, n, rank, const_cast<double*>(static_cast<const double*>(buf)), 1);
+  ALTO_LAUNCH_CHECK("alto_unpack_rows");
+  return ALTO_OK;
+}
+}  // extern "C"
