@@ -154,19 +154,28 @@ typedef struct alto_mttkrp_args {
    * tiles serialise in one L2 slice.  Their per-tile partials go instead to
    * `hot_copies` replicated buffers (tile % hot_copies), reduced into `out`
    * by a second kernel in a fixed order.  hot_slot: (I_mode,) int32, slot or
-   * -1; hot_rows: (n_hot,) int32; hot_buf: hot_copies * n_hot * rank float64,
-   * zero on entry and left zero on exit. */
+   * -1; hot_rows: (n_hot,) int32; hot_buf: hot_copies * n_hot * rank
+   * elements of out_dtype, zero on entry and left zero on exit (copies are
+   * summed in float64). */
   const int32_t* hot_slot;
   const int32_t* hot_rows;
   int32_t n_hot;
   int32_t hot_copies;
-  double* hot_buf;
+  void* hot_buf;
   int32_t flags;                 /* ALTO_STREAM_* tuning switches (0 = default) */
 } alto_mttkrp_args;
 
 /* Streaming-kernel tuning switches (alto_mttkrp_args.flags). */
 #define ALTO_STREAM_WARP_AGG 1   /* warp-aggregate in-tile sort atomics */
 #define ALTO_STREAM_FULL_BINS 2  /* scan all sort bins instead of the tile span */
+#define ALTO_STREAM_CTA_TILES 4  /* CTA-wide 1024-element tiles (cp.async staged)
+                                    instead of warp-autonomous 128-element tiles */
+#define ALTO_STREAM_GENERIC 128  /* bypass the specialised (order 3-5, rank 16/32) kernels */
+/* Ablation switches for profiling only (results are wrong when set). */
+#define ALTO_STREAM_DBG_NO_RED 8
+#define ALTO_STREAM_DBG_NO_GATHER 16
+#define ALTO_STREAM_DBG_NO_HOT 32
+#define ALTO_STREAM_DBG_NO_SORT 64
 
 /* Build the hot-row plan of one mode from its row pointer (alto_row_index):
  * rows with more than `tau` elements get slots (at most hmax);

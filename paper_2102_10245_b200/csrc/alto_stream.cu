@@ -5,22 +5,33 @@
 namespace alto {
 
 // Sum the replicated hot-row partials in copy order into out; re-zero them.
+// One thread per (hot row, rank) element; the copy loop is unrolled so 16
+// independent loads are in flight per thread (the copies live in L2).
 template <typename O>
-__global__ void hot_reduce_kernel(double* __restrict__ buf, const int* __restrict__ hot_rows, int n_hot, int copies,
-                                  int R, O* __restrict__ out) {
+__global__ void __launch_bounds__(256) hot_reduce_kernel(O* __restrict__ buf, const int* __restrict__ hot_rows,
+                                                         int n_hot, int copies, int R, O* __restrict__ out) {
   const long long n = static_cast<long long>(n_hot) * R;
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride) {
-    double s = 0.0;
-    for (int k = 0; k < copies; ++k) {
-      double* p = buf + k * n + i;
-      s += *p;
-      *p = 0.0;
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  int k = 0;
+  for (; k + 16 <= copies; k += 16) {
+    O v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = buf[(k + u) * n + i];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      s += static_cast<double>(v[u]);
+      buf[(k + u) * n + i] = O(0);
     }
-    const long long h = i / R;
-    O* o = out + static_cast<long long>(hot_rows[h]) * R + (i - h * R);
-    *o = static_cast<O>(static_cast<double>(*o) + s);
   }
+  for (; k < copies; ++k) {
+    s += static_cast<double>(buf[k * n + i]);
+    buf[k * n + i] = O(0);
+  }
+  const long long h = i / R;
+  O* o = out + static_cast<long long>(hot_rows[h]) * R + (i - h * R);
+  *o = static_cast<O>(static_cast<double>(*o) + s);
 }
 
 __global__ void hot_plan_kernel(const long long* __restrict__ row_ptr, long long dim, long long tau, int hmax,
@@ -92,18 +103,24 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.flags = a->flags;
   const auto* tab = static_cast<const uint64_t*>(a->d_tables);
   const bool o32 = a->out_dtype == ALTO_F32;
-  int st = d.n_words == 1 ? (o32 ? stream_w1_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
+  int st = d.n_words == 1 ? (o32 ? fast_w1_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
+                                 : fast_w1_f64(d, tab, P, a->value_dtype, a->factor_dtype, s))
+                          : (o32 ? fast_w2_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
+                                 : fast_w2_f64(d, tab, P, a->value_dtype, a->factor_dtype, s));
+  if (st == ALTO_EUNSUPPORTED)
+    st = d.n_words == 1 ? (o32 ? stream_w1_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
                                  : stream_w1_f64(d, tab, P, a->value_dtype, a->factor_dtype, s))
                           : (o32 ? stream_w2_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
                                  : stream_w2_f64(d, tab, P, a->value_dtype, a->factor_dtype, s));
   if (st) return st;
   if (P.n_hot > 0) {
-    const int grid = grid_for(static_cast<long long>(P.n_hot) * a->rank, 256);
+    const long long nh = static_cast<long long>(P.n_hot) * a->rank;
+    const int grid = static_cast<int>((nh + 255) / 256);
     if (a->out_dtype == ALTO_F32)
-      hot_reduce_kernel<float><<<grid, 256, 0, s>>>(P.hot_buf, a->hot_rows, P.n_hot, P.hot_copies, a->rank,
+      hot_reduce_kernel<float><<<grid, 256, 0, s>>>(static_cast<float*>(P.hot_buf), a->hot_rows, P.n_hot, P.hot_copies, a->rank,
                                                      static_cast<float*>(a->out));
     else
-      hot_reduce_kernel<double><<<grid, 256, 0, s>>>(P.hot_buf, a->hot_rows, P.n_hot, P.hot_copies, a->rank,
+      hot_reduce_kernel<double><<<grid, 256, 0, s>>>(static_cast<double*>(P.hot_buf), a->hot_rows, P.n_hot, P.hot_copies, a->rank,
                                                       static_cast<double*>(a->out));
     ALTO_LAUNCH_CHECK("alto_mttkrp/hot_reduce");
   }

@@ -56,7 +56,7 @@ struct StreamParams {
   long long ntiles;
   const int* hot_slot;
   int hot_copies;
-  double* hot_buf;
+  void* hot_buf;  // hot_copies x n_hot x R, element type = output type O
   int flags;  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
 };
 
@@ -94,6 +94,21 @@ __device__ __forceinline__ V4<F> gather4(const F* __restrict__ row, int r, int R
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) o.v[q] = (r + q < R) ? __ldg(row + r + q) : F(0);
+  }
+  return o;
+}
+
+// FULLR gather: the record holds the row's byte offset, so the address is one add.
+template <typename F>
+__device__ __forceinline__ V4<F> gather_off(const char* base, unsigned off) {
+  V4<F> o;
+  if constexpr (sizeof(F) == 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(base + off));
+    o.v[0] = t.x; o.v[1] = t.y; o.v[2] = t.z; o.v[3] = t.w;
+  } else {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(base + off));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(base + off) + 1);
+    o.v[0] = a.x; o.v[1] = a.y; o.v[2] = b.x; o.v[3] = b.y;
   }
   return o;
 }
@@ -195,10 +210,12 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
   const unsigned qmask = (G >= 4) ? (0xFu << (lane & ~3)) : 0xffffffffu;
   // input-mode factor bases in record order (mode skipped)
   const F* __restrict__ fin[NIN > 0 ? NIN : 1];
+  const char* fin_lane[NIN > 0 ? NIN : 1];  // fin[k] + this lane's first rank, as bytes
 #pragma unroll
   for (int k = 0; k < NIN; ++k) {
     const int n = k < mode ? k : k + 1;
     fin[k] = static_cast<const F*>(P.factors[n < ALTO_MAX_ORDER ? n : 0]);
+    fin_lane[k] = reinterpret_cast<const char*>(fin[k] + r_lane);
   }
   const V* __restrict__ vals = static_cast<const V*>(P.values);
   O* __restrict__ out = static_cast<O*>(P.out);
@@ -261,7 +278,11 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
           c[n] = n < N ? static_cast<unsigned>(packed_field<W>(p, L.pack_off[n], L.bits[n])) : 0u;
         const int row = static_cast<int>(pick<NMAX>(c, mode));
 #pragma unroll
-        for (int q = 0; q < NIN; ++q) rec[k][q] = (q < mode) ? c[q] : c[q + 1 < NMAX ? q + 1 : q];
+        for (int q = 0; q < NIN; ++q) {
+          const unsigned cq = (q < mode) ? c[q] : c[q + 1 < NMAX ? q + 1 : q];
+          // FULLR: byte offset of the factor row (fits in 32 bits, checked at launch)
+          rec[k][q] = FULLR ? cq * static_cast<unsigned>(4 * G * sizeof(F)) : cq;
+        }
         int tgt = row;
         if (hot_slot) {
           const int hs = __ldg(hot_slot + row);
@@ -374,10 +395,10 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
     }
     __syncthreads();
     // ---- phase B ------------------------------------------------------------
-    double* hot_base = P.n_hot > 0
-                           ? P.hot_buf + static_cast<long long>(static_cast<unsigned>(tile) & (P.hot_copies - 1)) *
-                                             P.n_hot * R
-                           : nullptr;
+    O* hot_base = P.n_hot > 0
+                      ? static_cast<O*>(P.hot_buf) +
+                            static_cast<long long>(static_cast<unsigned>(tile) & (P.hot_copies - 1)) * P.n_hot * R
+                      : nullptr;
     const int chunk = (cnt + NGROUPS - 1) / NGROUPS;
     const int j0 = grp * chunk;
     const int j1 = min(cnt, j0 + chunk);
@@ -396,7 +417,13 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
                             qmask, lane);
           }
         } else {
-          red_f64_sectors(hot_base + static_cast<long long>(-target - 1) * R, acc, r, R, G, qmask, lane);
+          if constexpr (sizeof(O) == 4) {
+            if (rank_ok) red_f32x4(reinterpret_cast<float*>(hot_base) + static_cast<long long>(-target - 1) * R, acc,
+                                   r, R, VEC);
+          } else {
+            red_f64_sectors(reinterpret_cast<double*>(hot_base) + static_cast<long long>(-target - 1) * R, acc, r, R,
+                            G, qmask, lane);
+          }
         }
       };
       auto block = [&](auto check_tag, int jb) {
@@ -425,7 +452,8 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
 #pragma unroll
             for (int k = 0; k < NIN; ++k)
               if ((NT > 0 || k < n_in) && rank_ok)
-                g[u][k] = gather4<F, VEC>(fin[k] + static_cast<unsigned long long>(cw[k]) * R, r, R);
+                g[u][k] = FULLR ? gather_off<F>(fin_lane[k], cw[k])
+                                : gather4<F, VEC>(fin[k] + static_cast<unsigned long long>(cw[k]) * R, r, R);
           }
         }
 #pragma unroll
@@ -479,6 +507,276 @@ stream_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ 
   }
 }
 
+// ---- warp-autonomous variant ------------------------------------------------
+// Each warp streams its own sub-tiles of kWarpTile consecutive elements:
+// coalesced key/value loads into registers, decode, a warp-private counting
+// sort by output row (bins + records in the warp's own smem slice), and the
+// same 4-lanes-per-element consumption as above — with only __syncwarp, so a
+// warp's decode/sort latency is hidden by the other warps instead of being
+// serialised behind CTA barriers.
+constexpr int kWarpTile = 128;   // elements per warp sub-tile (4 per lane)
+constexpr int kWarpBins = 512;   // warp-private sort bins
+
+template <int W, typename V, typename F, typename O, int NT, int G, bool VEC, bool FULLR>
+__global__ void __launch_bounds__(kTileThreads, 2)
+stream_warp_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ tab,
+                   const __grid_constant__ StreamParams P) {
+  using A = typename AccOf<V, F>::type;
+  constexpr int NMAX = NT > 0 ? NT : ALTO_MAX_ORDER;
+  using RL = RecLayout<NMAX, V>;
+  constexpr int NW = RL::NW;
+  constexpr int NIN = NMAX - 1;
+  constexpr int GPW = 32 / G;                    // element groups per warp
+  constexpr int CH = kWarpTile / GPW;            // records per group chunk
+  constexpr int U = 4;
+  constexpr int EPL = kWarpTile / 32;            // elements per lane in the load/decode pass
+  constexpr int REC_WORDS = kWarpTile * NW + GPW * 4;  // + swizzle headroom
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int N = NT > 0 ? NT : L.order;
+  const int R = P.rank;
+  const int mode = P.mode;
+  uint64_t* s_dec = reinterpret_cast<uint64_t*>(smem);
+  size_t off = (static_cast<size_t>(L.dec_bytes) * 256 * W * 8 + 15) & ~size_t(15);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned* s_rec = reinterpret_cast<unsigned*>(smem + off) + warp * (REC_WORDS + kWarpBins);
+  int* s_bin = reinterpret_cast<int*>(s_rec + REC_WORDS);
+
+  copy_to_smem(s_dec, tab + static_cast<long long>(L.dec_off) * W, L.dec_bytes * 256 * W);
+  __syncthreads();
+
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const int r_lane = 4 * gl;
+  const unsigned qmask = (G >= 4) ? (0xFu << (lane & ~3)) : 0xffffffffu;
+  const F* __restrict__ fin[NIN > 0 ? NIN : 1];
+  const char* fin_lane[NIN > 0 ? NIN : 1];
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) {
+    const int n = k < mode ? k : k + 1;
+    fin[k] = static_cast<const F*>(P.factors[n < ALTO_MAX_ORDER ? n : 0]);
+    fin_lane[k] = reinterpret_cast<const char*>(fin[k] + r_lane);
+  }
+  const V* __restrict__ vals = static_cast<const V*>(P.values);
+  O* __restrict__ out = static_cast<O*>(P.out);
+  const int* __restrict__ hot_slot = P.n_hot > 0 ? P.hot_slot : nullptr;
+  const int n_in = N - 1;
+  auto rec_addr = [&](int j) { return j * NW + (j / CH) * 4; };
+  const unsigned lt = (1u << lane) - 1u;
+  (void)lt;
+
+  const long long nsub = (P.m + kWarpTile - 1) / kWarpTile;
+  const long long gwarp = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp;
+  const long long nwarps = static_cast<long long>(gridDim.x) * (kTileThreads / 32);
+  for (long long sub = gwarp; sub < nsub; sub += nwarps) {
+    const long long e0 = sub * kWarpTile;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kWarpTile), P.m - e0));
+    // ---- load + decode (lane per element) --------------------------------
+    unsigned rec[EPL][NW];
+    int myrow[EPL];
+    Key<W> kk[EPL];
+    V vv0[EPL];
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const int e = lane + 32 * k;
+      if (e < cnt) {
+        kk[k] = load_key<W>(P.keys, e0 + e);
+        vv0[k] = __ldg(vals + e0 + e);
+      }
+    }
+    int lo = INT_MAX, hi = INT_MIN;
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const int e = lane + 32 * k;
+      myrow[k] = -1;
+      if (e < cnt) {
+        const Key<W> p = decode_packed<W>(s_dec, L.dec_bytes, kk[k]);
+        unsigned c[NMAX];
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n)
+          c[n] = n < N ? static_cast<unsigned>(packed_field<W>(p, L.pack_off[n], L.bits[n])) : 0u;
+        const int row = static_cast<int>(pick<NMAX>(c, mode));
+#pragma unroll
+        for (int q = 0; q < NIN; ++q) {
+          const unsigned cq = (q < mode) ? c[q] : c[q + 1 < NMAX ? q + 1 : q];
+          rec[k][q] = FULLR ? cq * static_cast<unsigned>(4 * G * sizeof(F)) : cq;
+        }
+        int tgt = row;
+        if (hot_slot && !(P.flags & ALTO_STREAM_DBG_NO_HOT)) {
+          const int hs = __ldg(hot_slot + row);
+          if (hs >= 0) tgt = -(hs + 1);
+        }
+        rec[k][RL::TGT] = static_cast<unsigned>(tgt);
+        if constexpr (sizeof(V) == 4) {
+          rec[k][RL::VAL] = __float_as_uint(static_cast<float>(vv0[k]));
+        } else {
+          const unsigned long long u = __double_as_longlong(static_cast<double>(vv0[k]));
+          rec[k][RL::VAL] = static_cast<unsigned>(u);
+          rec[k][RL::VAL + 1] = static_cast<unsigned>(u >> 32);
+        }
+#pragma unroll
+        for (int q = RL::raw; q < NW; ++q) rec[k][q] = 0u;
+        myrow[k] = row;
+        lo = min(lo, row);
+        hi = max(hi, row);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int span = hi - lo + 1;
+    // ---- warp-private counting sort by output row ------------------------
+    if (span <= kWarpBins && !(P.flags & ALTO_STREAM_DBG_NO_SORT)) {
+      for (int i = lane; i < span; i += 32) s_bin[i] = 0;
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < EPL; ++k)
+        if (myrow[k] >= 0) atomicAdd(&s_bin[myrow[k] - lo], 1);
+      __syncwarp();
+      const int per = (span + 31) / 32;
+      const int b0 = min(span, lane * per), b1 = min(span, b0 + per);
+      int sum = 0;
+      for (int i = b0; i < b1; ++i) sum += s_bin[i];
+      int x = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int run = x - sum;
+      for (int i = b0; i < b1; ++i) {
+        const int c = s_bin[i];
+        s_bin[i] = run;
+        run += c;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < EPL; ++k)
+        if (myrow[k] >= 0) {
+          const int slot = atomicAdd(&s_bin[myrow[k] - lo], 1);
+#pragma unroll
+          for (int q = 0; q < NW; q += 4)
+            *reinterpret_cast<uint4*>(s_rec + rec_addr(slot) + q) =
+                make_uint4(rec[k][q], rec[k][q + 1], rec[k][q + 2], rec[k][q + 3]);
+        }
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPL; ++k)
+        if (myrow[k] >= 0) {
+          const int e = lane + 32 * k;
+#pragma unroll
+          for (int q = 0; q < NW; q += 4)
+            *reinterpret_cast<uint4*>(s_rec + rec_addr(e) + q) =
+                make_uint4(rec[k][q], rec[k][q + 1], rec[k][q + 2], rec[k][q + 3]);
+        }
+    }
+    __syncwarp();
+    // ---- consume: G lanes per element ------------------------------------
+    O* hot_base = P.n_hot > 0
+                      ? static_cast<O*>(P.hot_buf) +
+                            static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) * P.n_hot * R
+                      : nullptr;
+    const int j0 = grp * CH;
+    const int j1 = min(cnt, j0 + CH);
+    for (int r0 = 0; r0 < (FULLR ? 4 * G : R); r0 += 4 * G) {
+      const int r = r0 + r_lane;
+      const bool rank_ok = FULLR || r < R;
+      A acc[4] = {A(0), A(0), A(0), A(0)};
+      int cur = INT_MIN;
+      auto flush = [&](int target) {
+        O* base = target >= 0 ? out + static_cast<long long>(target) * R
+                              : hot_base + static_cast<long long>(-target - 1) * R;
+        if (P.flags & ALTO_STREAM_DBG_NO_RED) {
+          if (acc[0] == A(-12345.678)) out[0] = O(1);  // keep the math alive
+          return;
+        }
+        if constexpr (sizeof(O) == 4) {
+          if (rank_ok) red_f32x4(reinterpret_cast<float*>(base), acc, r, R, VEC);
+        } else {
+          red_f64_sectors(reinterpret_cast<double*>(base), acc, r, R, G, qmask, lane);
+        }
+      };
+      for (int jb = j0; jb < j1; jb += U) {
+        int tg[U];
+        A vv[U];
+        V4<F> g[U][NIN > 0 ? NIN : 1];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = jb + u;
+          tg[u] = INT_MIN;
+          if (j < j1) {
+            unsigned cw[NW];
+#pragma unroll
+            for (int q = 0; q < NW; q += 4) {
+              const uint4 t = *reinterpret_cast<const uint4*>(s_rec + rec_addr(j) + q);
+              cw[q] = t.x; cw[q + 1] = t.y; cw[q + 2] = t.z; cw[q + 3] = t.w;
+            }
+            tg[u] = static_cast<int>(cw[RL::TGT]);
+            if constexpr (sizeof(V) == 4) {
+              vv[u] = static_cast<A>(__uint_as_float(cw[RL::VAL]));
+            } else {
+              vv[u] = static_cast<A>(__longlong_as_double(static_cast<long long>(
+                  (static_cast<unsigned long long>(cw[RL::VAL + 1]) << 32) | cw[RL::VAL])));
+            }
+#pragma unroll
+            for (int k = 0; k < NIN; ++k)
+              if ((NT > 0 || k < n_in) && rank_ok) {
+                if (P.flags & ALTO_STREAM_DBG_NO_GATHER) {
+                  const float z = __uint_as_float(cw[k] & 0x3f800000u);
+                  g[u][k].v[0] = g[u][k].v[1] = g[u][k].v[2] = g[u][k].v[3] = static_cast<F>(z);
+                } else {
+                  g[u][k] = FULLR ? gather_off<F>(fin_lane[k], cw[k])
+                                  : gather4<F, VEC>(fin[k] + static_cast<unsigned long long>(cw[k]) * R, r, R);
+                }
+              }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (tg[u] == INT_MIN) continue;
+          A t[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) t[q] = vv[u];
+          int last = -1;
+          if (rank_ok) {
+#pragma unroll
+            for (int k = 0; k < NIN; ++k)
+              if (NT > 0 || k < n_in) last = k;
+#pragma unroll
+            for (int k = 0; k < NIN; ++k)
+              if ((NT > 0 || k < n_in) && k != last) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) t[q] *= static_cast<A>(g[u][k].v[q]);
+              }
+          }
+          if (tg[u] == cur) {
+            if (last >= 0) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[q] = fma(t[q], static_cast<A>(g[u][last].v[q]), acc[q]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[q] += t[q];
+            }
+          } else {
+            if (cur != INT_MIN) flush(cur);
+            if (last >= 0) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[q] = t[q] * static_cast<A>(g[u][last].v[q]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[q] = t[q];
+            }
+            cur = tg[u];
+          }
+        }
+      }
+      if (cur != INT_MIN) flush(cur);
+    }
+    __syncwarp();
+  }
+}
+
 // ---- launch ---------------------------------------------------------------------
 
 template <typename K>
@@ -502,15 +800,30 @@ template <int W, typename V, typename F, typename O, int NT, int G, bool VEC, bo
 int launch(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaStream_t s) {
   constexpr int NMAX = NT > 0 ? NT : ALTO_MAX_ORDER;
   constexpr int NW = RecLayout<NMAX, V>::NW;
-  const size_t stage_bytes = (static_cast<size_t>(P.tile) * (W * 8 + sizeof(V)) + 15) & ~size_t(15);
-  const size_t smem = ((static_cast<size_t>(d.dec_bytes) * 256 * W * 8 + 15) & ~size_t(15)) +
-                      static_cast<size_t>(P.tile) * NW * 4 + kRecPad * 4 +
-                      (((kSortBins + kTileWarps) * sizeof(int) + 15) & ~size_t(15)) + 2 * stage_bytes;
-  auto kern = stream_kernel<W, V, F, O, NT, G, VEC, FULLR>;
+  const size_t dec = (static_cast<size_t>(d.dec_bytes) * 256 * W * 8 + 15) & ~size_t(15);
+  if (P.flags & ALTO_STREAM_CTA_TILES) {
+    const size_t stage_bytes = (static_cast<size_t>(P.tile) * (W * 8 + sizeof(V)) + 15) & ~size_t(15);
+    const size_t smem = dec + static_cast<size_t>(P.tile) * NW * 4 + kRecPad * 4 +
+                        (((kSortBins + kTileWarps) * sizeof(int) + 15) & ~size_t(15)) + 2 * stage_bytes;
+    auto kern = stream_kernel<W, V, F, O, NT, G, VEC, FULLR>;
+    if (prep(kern, smem)) return ALTO_ECUDA;
+    int bps = 1;
+    ALTO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kTileThreads, smem));
+    const long long grid = std::min<long long>(P.ntiles, static_cast<long long>(device_sms()) * std::max(bps, 1));
+    kern<<<static_cast<unsigned>(grid), kTileThreads, smem, s>>>(d, tab, P);
+    ALTO_LAUNCH_CHECK("alto_mttkrp");
+    return ALTO_OK;
+  }
+  constexpr int GPW = 32 / G;
+  const size_t per_warp = (static_cast<size_t>(kWarpTile) * NW + GPW * 4 + kWarpBins) * 4;
+  const size_t smem = dec + (kTileThreads / 32) * per_warp;
+  auto kern = stream_warp_kernel<W, V, F, O, NT, G, VEC, FULLR>;
   if (prep(kern, smem)) return ALTO_ECUDA;
   int bps = 1;
   ALTO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kTileThreads, smem));
-  const long long grid = std::min<long long>(P.ntiles, static_cast<long long>(device_sms()) * std::max(bps, 1));
+  const long long nsub = (P.m + kWarpTile - 1) / kWarpTile;
+  const long long need = (nsub + kTileThreads / 32 - 1) / (kTileThreads / 32);
+  const long long grid = std::min<long long>(need, static_cast<long long>(device_sms()) * std::max(bps, 1));
   kern<<<static_cast<unsigned>(grid), kTileThreads, smem, s>>>(d, tab, P);
   ALTO_LAUNCH_CHECK("alto_mttkrp");
   return ALTO_OK;
@@ -519,8 +832,12 @@ int launch(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaS
 template <int W, typename V, typename F, typename O, int NT>
 int by_rank(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaStream_t s) {
   const int groups = (P.rank + 3) / 4;
-  if (P.rank == 16) return launch<W, V, F, O, NT, 4, true, true>(d, tab, P, s);
-  if (P.rank == 32) return launch<W, V, F, O, NT, 8, true, true>(d, tab, P, s);
+  // FULLR kernels keep 32-bit row byte offsets in the records
+  long long maxdim = 0;
+  for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
+  const bool off32 = maxdim * P.rank * static_cast<long long>(sizeof(F)) <= 0xFFFFFFFFll;
+  if (off32 && P.rank == 16) return launch<W, V, F, O, NT, 4, true, true>(d, tab, P, s);
+  if (off32 && P.rank == 32) return launch<W, V, F, O, NT, 8, true, true>(d, tab, P, s);
   if (P.rank % 4 == 0) {
     if (groups <= 1) return launch<W, V, F, O, NT, 1, true, false>(d, tab, P, s);
     if (groups <= 2) return launch<W, V, F, O, NT, 2, true, false>(d, tab, P, s);
@@ -542,7 +859,13 @@ int by_order(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cud
   }
 }
 
-// per-translation-unit entry points (alto_stream_w{1,2}_{f32,f64}.cu)
+// per-translation-unit entry points (alto_stream_w{1,2}_{f32,f64}.cu, and the
+// specialised kernels of alto_fast_w{1,2}_{f32,f64}.cu, which return
+// ALTO_EUNSUPPORTED without launching when the shape is not covered)
+int fast_w1_f32(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
+int fast_w1_f64(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
+int fast_w2_f32(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
+int fast_w2_f64(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
 int stream_w1_f32(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
 int stream_w1_f64(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
 int stream_w2_f32(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);

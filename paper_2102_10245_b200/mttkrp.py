@@ -119,13 +119,15 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
 # contending on one L2 line (see alto_mttkrp_args in include/alto_b200.h).
 HOT_TAU = 1024
 HOT_MAX = 8192
-HOT_COPIES = 32
+# float32 copies take fewer adds each (precision); float64 copies fewer bytes
+HOT_COPIES = {4: 128, 8: 32}
 
 
-def hot_plan(tensor: AltoTensor, mode: int, rank: int):
-    """Per-(mode, rank) hot-row plan, built once from the row index and cached."""
+def hot_plan(tensor: AltoTensor, mode: int, rank: int, out_dtype=None):
+    """Per-(mode, rank, output dtype) hot-row plan, built once from the row index and cached."""
     torch = _torch()
-    key = ("hot", mode, rank)
+    out_dtype = out_dtype or torch.float64
+    key = ("hot", mode, rank, out_dtype)
     if key in tensor._cache:
         return tensor._cache[key]
     lib = _lib.load()
@@ -143,8 +145,9 @@ def hot_plan(tensor: AltoTensor, mode: int, rank: int):
     n = int(nhot.item())
     plan = None
     if n > 0:
-        buf = torch.zeros(HOT_COPIES * n * rank, dtype=torch.float64, device=dev)
-        plan = (slot, rows, n, HOT_COPIES, buf)
+        copies = HOT_COPIES[torch.empty(0, dtype=out_dtype).element_size()]
+        buf = torch.zeros(copies * n * rank, dtype=out_dtype, device=dev)
+        plan = (slot, rows, n, copies, buf)
     tensor._cache[key] = plan
     return plan
 
@@ -161,7 +164,7 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
     if out is None:
         out = torch.empty((dim, rank), dtype=out_dtype or torch.float64, device=tensor.keys.device)
     a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
-    hp = hot_plan(tensor, mode, rank) if hot else None
+    hp = hot_plan(tensor, mode, rank, out.dtype) if hot else None
     if hp is not None:
         slot, rows, n, copies, buf = hp
         a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf = (slot.data_ptr(), rows.data_ptr(), n, copies,
