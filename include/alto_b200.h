@@ -171,6 +171,8 @@ typedef struct alto_mttkrp_args {
 #define ALTO_STREAM_CTA_TILES 4  /* CTA-wide 1024-element tiles (cp.async staged)
                                     instead of warp-autonomous 128-element tiles */
 #define ALTO_STREAM_GENERIC 128  /* bypass the specialised (order 3-5, rank 16/32) kernels */
+#define ALTO_STREAM_TUNE_MINB2 256  /* tuning: 2 CTAs/SM launch bounds (default 3) */
+#define ALTO_STREAM_TUNE_U4 512     /* tuning: 4 elements in flight per group (default 2) */
 /* Ablation switches for profiling only (results are wrong when set). */
 #define ALTO_STREAM_DBG_NO_RED 8
 #define ALTO_STREAM_DBG_NO_GATHER 16

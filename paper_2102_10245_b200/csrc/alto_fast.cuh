@@ -55,8 +55,8 @@ __device__ __forceinline__ unsigned fast_field(const unsigned (&p)[2 * W], int o
   return nb >= 32 ? v : (v & ((1u << nb) - 1u));
 }
 
-template <int W, typename V, typename O, int N, int R>
-__global__ void __launch_bounds__(kTileThreads, 2)
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int UF = 2>
+__global__ void __launch_bounds__(kTileThreads, MINB)
 fast_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ tab,
             const __grid_constant__ StreamParams P) {
   using F = V;
@@ -68,7 +68,7 @@ fast_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ ta
   using RL = RecLayout<N, V>;
   constexpr int NW = RL::NW;
   constexpr int EPL = kFastTile / 32;
-  constexpr int U = 4;
+  constexpr int U = UF;
   constexpr int REC_WORDS = kFastTile * NW + GPW * 4;
   extern __shared__ __align__(16) unsigned char smem[];
   const int mode = P.mode;
@@ -183,36 +183,46 @@ fast_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ ta
     if (span <= kFastBins) {
       for (int i = lane; i < span; i += 32) s_bin[i] = 0;
       __syncwarp();
+      // histogram: one atomic per group of equal rows (hot rows repeat a lot)
+      unsigned peers[EPL];
+      const unsigned ltm = (1u << lane) - 1u;
 #pragma unroll
-      for (int k = 0; k < EPL; ++k)
-        if (myrow[k] >= 0) atomicAdd(&s_bin[myrow[k] - lo], 1);
-      __syncwarp();
-      const int per = (span + 31) >> 5;
-      const int b0 = min(span, lane * per), b1 = min(span, b0 + per);
-      int sum = 0;
-      for (int i = b0; i < b1; ++i) sum += s_bin[i];
-      int x = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      int run = x - sum;
-      for (int i = b0; i < b1; ++i) {
-        const int c = s_bin[i];
-        s_bin[i] = run;
-        run += c;
+      for (int k = 0; k < EPL; ++k) {
+        const bool ok = myrow[k] >= 0;
+        peers[k] = __match_any_sync(0xffffffffu, ok ? myrow[k] : -1 - lane);
+        if (ok && (peers[k] & ltm) == 0) atomicAdd(&s_bin[myrow[k] - lo], __popc(peers[k]));
       }
       __syncwarp();
+      // exclusive scan over the span in conflict-free 32-bin rounds
+      int carry = 0;
+      for (int base = 0; base < span; base += 32) {
+        const int i = base + lane;
+        const int v = i < span ? s_bin[i] : 0;
+        int x = v;
 #pragma unroll
-      for (int k = 0; k < EPL; ++k)
-        if (myrow[k] >= 0) {
-          const int slot = atomicAdd(&s_bin[myrow[k] - lo], 1);
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (i < span) s_bin[i] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < EPL; ++k) {
+        const bool ok = myrow[k] >= 0;
+        const int leader = __ffs(peers[k]) - 1;
+        int basev = 0;
+        if (ok && leader == lane) basev = atomicAdd(&s_bin[myrow[k] - lo], __popc(peers[k]));
+        basev = __shfl_sync(0xffffffffu, basev, leader);
+        if (ok) {
+          const int slot = basev + __popc(peers[k] & ltm);
 #pragma unroll
           for (int q = 0; q < NW; q += 4)
             *reinterpret_cast<uint4*>(s_rec + rec_addr(slot) + q) =
                 make_uint4(rec[k][q], rec[k][q + 1], rec[k][q + 2], rec[k][q + 3]);
         }
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < EPL; ++k)
@@ -305,13 +315,13 @@ fast_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ ta
   }
 }
 
-template <int W, typename V, typename O, int N, int R>
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int UF = 2>
 int launch_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaStream_t s) {
   constexpr int NW = RecLayout<N, V>::NW;
   constexpr int GPW = 32 / (R / 4);
   const size_t dec = (static_cast<size_t>(d.dec_bytes) * 256 * W * 8 + 15) & ~size_t(15);
   const size_t smem = dec + (kTileThreads / 32) * (static_cast<size_t>(kFastTile) * NW + GPW * 4 + kFastBins) * 4;
-  auto kern = fast_kernel<W, V, O, N, R>;
+  auto kern = fast_kernel<W, V, O, N, R, MINB, UF>;
   // launch configuration cached per instantiation and shared-memory size
   static size_t cached_smem = 0;
   static int cached_bps = 0;
@@ -341,6 +351,13 @@ int try_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cud
   for (int n = 0; n < d.order; ++n)
     if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
   if (P.rank == 16) {
+    if constexpr (W == 1 && sizeof(V) == 4 && sizeof(O) == 4) {
+      // tuning variants (ALTO_STREAM_TUNE_* flags), cfg2 shape only
+      if (d.order == 3 && (P.flags & ALTO_STREAM_TUNE_MINB2) && (P.flags & ALTO_STREAM_TUNE_U4))
+        return launch_fast<W, V, O, 3, 16, 2, 4>(d, tab, P, s);
+      if (d.order == 3 && (P.flags & ALTO_STREAM_TUNE_MINB2)) return launch_fast<W, V, O, 3, 16, 2, 2>(d, tab, P, s);
+      if (d.order == 3 && (P.flags & ALTO_STREAM_TUNE_U4)) return launch_fast<W, V, O, 3, 16, 3, 4>(d, tab, P, s);
+    }
     if (d.order == 3) return launch_fast<W, V, O, 3, 16>(d, tab, P, s);
     if (d.order == 4) return launch_fast<W, V, O, 4, 16>(d, tab, P, s);
     if (d.order == 5) return launch_fast<W, V, O, 5, 16>(d, tab, P, s);

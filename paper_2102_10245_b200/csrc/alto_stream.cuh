@@ -836,8 +836,7 @@ int by_rank(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cuda
   long long maxdim = 0;
   for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
   const bool off32 = maxdim * P.rank * static_cast<long long>(sizeof(F)) <= 0xFFFFFFFFll;
-  if (off32 && P.rank == 16) return launch<W, V, F, O, NT, 4, true, true>(d, tab, P, s);
-  if (off32 && P.rank == 32) return launch<W, V, F, O, NT, 8, true, true>(d, tab, P, s);
+  (void)off32;
   if (P.rank % 4 == 0) {
     if (groups <= 1) return launch<W, V, F, O, NT, 1, true, false>(d, tab, P, s);
     if (groups <= 2) return launch<W, V, F, O, NT, 2, true, false>(d, tab, P, s);
@@ -851,12 +850,9 @@ int by_rank(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cuda
 
 template <int W, typename V, typename F, typename O>
 int by_order(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaStream_t s) {
-  switch (d.order) {
-    case 3: return by_rank<W, V, F, O, 3>(d, tab, P, s);
-    case 4: return by_rank<W, V, F, O, 4>(d, tab, P, s);
-    case 5: return by_rank<W, V, F, O, 5>(d, tab, P, s);
-    default: return by_rank<W, V, F, O, 0>(d, tab, P, s);
-  }
+  // Generic fallback: runtime order (the specialised order-3/4/5, rank-16/32
+  // kernels live in alto_fast.cuh).
+  return by_rank<W, V, F, O, 0>(d, tab, P, s);
 }
 
 // per-translation-unit entry points (alto_stream_w{1,2}_{f32,f64}.cu, and the
