@@ -163,7 +163,25 @@ typedef struct alto_mttkrp_args {
   int32_t hot_copies;
   void* hot_buf;
   int32_t flags;                 /* ALTO_STREAM_* tuning switches (0 = default) */
+  /* Optional per-tensor / per-mode plan (BLCO-style): `packed` holds every
+   * key bit-permuted so each mode's bits are contiguous (same bits, same
+   * element order; alto_pack_keys) and `pos` each element's row-sorted slot
+   * in its 128-element sub-tile for this mode (alto_subtile_order).  With
+   * both set, the specialised kernels skip the byte-table decode and the
+   * in-tile sort. */
+  const uint64_t* packed;
+  const uint8_t* pos;
 } alto_mttkrp_args;
+
+/* Mode-contiguous re-encoding of sorted ALTO keys: packed[i] holds mode n's
+ * coordinate in bits [sum_{m<n} b_m, +b_n) (same n_words as the keys). */
+int alto_pack_keys(const alto_layout* lay, const void* d_tables, const uint64_t* keys, int64_t m,
+                   uint64_t* packed, void* stream);
+/* Per-mode sub-tile order: pos[i] = slot of element i inside its 128-element
+ * sub-tile after a stable counting sort by its `mode` coordinate (identity
+ * for sub-tiles whose rows span more than 512). */
+int alto_subtile_order(const alto_layout* lay, const uint64_t* packed, int64_t m, int32_t mode, uint8_t* pos,
+                       void* stream);
 
 /* Streaming-kernel tuning switches (alto_mttkrp_args.flags). */
 #define ALTO_STREAM_WARP_AGG 1   /* warp-aggregate in-tile sort atomics */

@@ -55,6 +55,8 @@ class CMttkrpArgs(Structure):
         ("hot_copies", c_int32),
         ("hot_buf", c_void_p),
         ("flags", c_int32),
+        ("packed", c_void_p),
+        ("pos", c_void_p),
     ]
 
 
@@ -80,6 +82,8 @@ SIGNATURES = [
     ("alto_tile_intervals", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                       c_void_p]),
     ("alto_mttkrp", c_int32, [POINTER(CMttkrpArgs), c_void_p]),
+    ("alto_pack_keys", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    ("alto_subtile_order", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_hot_plan", c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("alto_row_index_workspace_bytes", c_size_t, [c_int64, c_int64]),
     ("alto_row_index", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,

@@ -343,8 +343,16 @@ int launch_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, 
 
 // Returns ALTO_EUNSUPPORTED (without launching) when the shape is not covered.
 template <int W, typename V, typename O>
+int try_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packed, const unsigned char* pos,
+                cudaStream_t s);
+
+template <int W, typename V, typename O>
 int try_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaStream_t s) {
   if (P.flags & (ALTO_STREAM_CTA_TILES | ALTO_STREAM_GENERIC)) return ALTO_EUNSUPPORTED;
+  if (P.packed && P.pos) {
+    const int st = try_planned<W, V, O>(d, P, P.packed, P.pos, s);
+    if (st != ALTO_EUNSUPPORTED) return st;
+  }
   long long maxdim = 0;
   for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
   if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
@@ -366,6 +374,257 @@ int try_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cud
     if (d.order == 3) return launch_fast<W, V, O, 3, 32>(d, tab, P, s);
     if (d.order == 4) return launch_fast<W, V, O, 4, 32>(d, tab, P, s);
     if (d.order == 5) return launch_fast<W, V, O, 5, 32>(d, tab, P, s);
+  }
+  return ALTO_EUNSUPPORTED;
+}
+
+
+// ---- planned variant: mode-contiguous keys + precomputed sub-tile order --------
+// Built once per tensor (packed keys) and per mode (positions) — see
+// alto_pack_keys / alto_subtile_order.  The packed key is the ALTO key with
+// its bits permuted so that mode n occupies bits [pack_off[n], +bits[n]):
+// same bits, same element order, decode = one funnel shift + mask per mode.
+// pos[e] is element e's slot in its 128-element sub-tile after a stable
+// counting sort by output row (identity when the sub-tile's rows span more
+// than kFastBins), so phase A scatters records without any sorting work.
+
+template <int W>
+__device__ __forceinline__ unsigned packed_field32(const Key<W>& k, int off, int nb) {
+  unsigned w[2 * W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    w[2 * i] = static_cast<unsigned>(k.w[i]);
+    w[2 * i + 1] = static_cast<unsigned>(k.w[i] >> 32);
+  }
+  return fast_field<W>(w, off, nb);
+}
+
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int UF = 2>
+__global__ void __launch_bounds__(kTileThreads, MINB)
+planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ packed,
+               const unsigned char* __restrict__ pos, const __grid_constant__ StreamParams P) {
+  using F = V;
+  using A = V;
+  constexpr int G = R / 4;
+  constexpr int GPW = 32 / G;
+  constexpr int CH = kFastTile / GPW;
+  constexpr int NIN = N - 1;
+  using RL = RecLayout<N, V>;
+  constexpr int NW = RL::NW;
+  constexpr int EPL = kFastTile / 32;
+  constexpr int U = UF;
+  constexpr int REC_WORDS = kFastTile * NW + GPW * 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int mode = P.mode;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned* s_rec = reinterpret_cast<unsigned*>(smem) + warp * REC_WORDS;
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const unsigned qmask = (G >= 4) ? (0xFu << (lane & ~3)) : 0xffffffffu;
+  const char* fin_lane[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) {
+    const int n = k < mode ? k : k + 1;
+    fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(P.factors[n]) + 4 * gl);
+  }
+  int pack_off[N], bits[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) { pack_off[n] = L.pack_off[n]; bits[n] = L.bits[n]; }
+  const V* __restrict__ vals = static_cast<const V*>(P.values);
+  O* __restrict__ out = static_cast<O*>(P.out);
+  const int* __restrict__ hot_slot = P.n_hot > 0 ? P.hot_slot : nullptr;
+  constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
+  auto rec_addr = [](int j) { return j * NW + (j / CH) * 4; };
+
+  const long long nsub = (P.m + kFastTile - 1) / kFastTile;
+  const long long gw0 = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp;
+  const long long nwarps = static_cast<long long>(gridDim.x) * (kTileThreads / 32);
+  Key<W> nk[EPL];
+  V nv[EPL];
+  unsigned char np[EPL];
+  auto prefetch = [&](long long sb) {
+    if (sb >= nsub) return;
+    const long long b0 = sb * kFastTile;
+    const int c = static_cast<int>(min(static_cast<long long>(kFastTile), P.m - b0));
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const int e = lane + 32 * k;
+      if (e < c) {
+        nk[k] = load_key<W>(packed, b0 + e);
+        nv[k] = __ldg(vals + b0 + e);
+        np[k] = __ldg(pos + b0 + e);
+      }
+    }
+  };
+  prefetch(gw0);
+  for (long long sub = gw0; sub < nsub; sub += nwarps) {
+    const long long e0 = sub * kFastTile;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kFastTile), P.m - e0));
+    Key<W> kk[EPL];
+    V vv0[EPL];
+    unsigned char pp[EPL];
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) { kk[k] = nk[k]; vv0[k] = nv[k]; pp[k] = np[k]; }
+    prefetch(sub + nwarps);
+    // ---- records straight to their sorted slots ------------------------------
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const int e = lane + 32 * k;
+      if (e < cnt) {
+        unsigned c[N];
+#pragma unroll
+        for (int n = 0; n < N; ++n) c[n] = packed_field32<W>(kk[k], pack_off[n], bits[n]);
+        unsigned row = c[0];
+#pragma unroll
+        for (int n = 1; n < N; ++n)
+          if (n == mode) row = c[n];
+        unsigned rec[NW];
+#pragma unroll
+        for (int q = 0; q < NIN; ++q) rec[q] = ((q < mode) ? c[q] : c[q + 1]) * ROWB;
+        int tgt = static_cast<int>(row);
+        if (hot_slot) {
+          const int hs = __ldg(hot_slot + row);
+          if (hs >= 0) tgt = -(hs + 1);
+        }
+        rec[RL::TGT] = static_cast<unsigned>(tgt);
+        if constexpr (sizeof(V) == 4) {
+          rec[RL::VAL] = __float_as_uint(vv0[k]);
+        } else {
+          const unsigned long long u = __double_as_longlong(vv0[k]);
+          rec[RL::VAL] = static_cast<unsigned>(u);
+          rec[RL::VAL + 1] = static_cast<unsigned>(u >> 32);
+        }
+#pragma unroll
+        for (int q = RL::raw; q < NW; ++q) rec[q] = 0u;
+        const int slot = pp[k];
+#pragma unroll
+        for (int q = 0; q < NW; q += 4)
+          *reinterpret_cast<uint4*>(s_rec + rec_addr(slot) + q) = make_uint4(rec[q], rec[q + 1], rec[q + 2], rec[q + 3]);
+      }
+    }
+    __syncwarp();
+    // ---- consume (identical to fast_kernel) -------------------------------------
+    O* hot_base = hot_slot ? static_cast<O*>(P.hot_buf) +
+                                 static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) * P.n_hot * R
+                           : nullptr;
+    A acc[4] = {A(0), A(0), A(0), A(0)};
+    int cur = INT_MIN;
+    auto flush = [&]() {
+      O* base = cur >= 0 ? out + static_cast<long long>(cur) * R : hot_base + static_cast<long long>(-cur - 1) * R;
+      if constexpr (sizeof(O) == 4) {
+        red_f32x4(reinterpret_cast<float*>(base), acc, 4 * gl, R, true);
+      } else {
+        red_f64_sectors(reinterpret_cast<double*>(base), acc, 4 * gl, R, G, qmask, lane);
+      }
+    };
+    auto consume = [&](const unsigned (&cw)[NW], const V4<F> (&g)[NIN]) {
+      const int tg = static_cast<int>(cw[RL::TGT]);
+      A v;
+      if constexpr (sizeof(V) == 4) {
+        v = __uint_as_float(cw[RL::VAL]);
+      } else {
+        v = __longlong_as_double(
+            static_cast<long long>((static_cast<unsigned long long>(cw[RL::VAL + 1]) << 32) | cw[RL::VAL]));
+      }
+      A t[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) t[q] = v * static_cast<A>(g[0].v[q]);
+#pragma unroll
+      for (int k = 1; k < NIN - 1; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t[q] *= static_cast<A>(g[k].v[q]);
+      if (tg == cur) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = fma(t[q], static_cast<A>(g[NIN - 1].v[q]), acc[q]);
+      } else {
+        if (cur != INT_MIN) flush();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = t[q] * static_cast<A>(g[NIN - 1].v[q]);
+        cur = tg;
+      }
+    };
+    const int j0 = grp * CH;
+    if (cnt == kFastTile) {
+#pragma unroll 1
+      for (int jb = j0; jb < j0 + CH; jb += U) {
+        unsigned cw[U][NW];
+        V4<F> g[U][NIN];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int q = 0; q < NW; q += 4) {
+            const uint4 t = *reinterpret_cast<const uint4*>(s_rec + rec_addr(jb + u) + q);
+            cw[u][q] = t.x; cw[u][q + 1] = t.y; cw[u][q + 2] = t.z; cw[u][q + 3] = t.w;
+          }
+#pragma unroll
+          for (int k = 0; k < NIN; ++k) g[u][k] = gather_off<F>(fin_lane[k], cw[u][k]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) consume(cw[u], g[u]);
+      }
+    } else {
+      const int j1 = min(cnt, j0 + CH);
+#pragma unroll 1
+      for (int j = j0; j < j1; ++j) {
+        unsigned cw[NW];
+        V4<F> g[NIN];
+#pragma unroll
+        for (int q = 0; q < NW; q += 4) {
+          const uint4 t = *reinterpret_cast<const uint4*>(s_rec + rec_addr(j) + q);
+          cw[q] = t.x; cw[q + 1] = t.y; cw[q + 2] = t.z; cw[q + 3] = t.w;
+        }
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) g[k] = gather_off<F>(fin_lane[k], cw[k]);
+        consume(cw, g);
+      }
+    }
+    if (cur != INT_MIN) flush();
+    __syncwarp();
+  }
+}
+
+template <int W, typename V, typename O, int N, int R>
+int launch_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packed, const unsigned char* pos,
+                   cudaStream_t s) {
+  constexpr int NW = RecLayout<N, V>::NW;
+  constexpr int GPW = 32 / (R / 4);
+  const size_t smem = (kTileThreads / 32) * (static_cast<size_t>(kFastTile) * NW + GPW * 4) * 4;
+  auto kern = planned_kernel<W, V, O, N, R>;
+  static size_t cached_smem = 0;
+  static int cached_bps = 0;
+  if (cached_smem != smem) {
+    if (prep(kern, smem)) return ALTO_ECUDA;
+    int b = 1;
+    ALTO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kTileThreads, smem));
+    cached_bps = b;
+    cached_smem = smem;
+  }
+  const long long nsub = (P.m + kFastTile - 1) / kFastTile;
+  const long long need = (nsub + kTileThreads / 32 - 1) / (kTileThreads / 32);
+  const long long grid = std::min<long long>(need, static_cast<long long>(device_sms()) * std::max(cached_bps, 1));
+  kern<<<static_cast<unsigned>(grid), kTileThreads, smem, s>>>(d, packed, pos, P);
+  ALTO_LAUNCH_CHECK("alto_mttkrp(planned)");
+  return ALTO_OK;
+}
+
+template <int W, typename V, typename O>
+int try_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packed, const unsigned char* pos,
+                cudaStream_t s) {
+  if (!packed || !pos || (P.flags & (ALTO_STREAM_CTA_TILES | ALTO_STREAM_GENERIC))) return ALTO_EUNSUPPORTED;
+  long long maxdim = 0;
+  for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
+  if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
+  for (int n = 0; n < d.order; ++n)
+    if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
+  if (P.rank == 16) {
+    if (d.order == 3) return launch_planned<W, V, O, 3, 16>(d, P, packed, pos, s);
+    if (d.order == 4) return launch_planned<W, V, O, 4, 16>(d, P, packed, pos, s);
+    if (d.order == 5) return launch_planned<W, V, O, 5, 16>(d, P, packed, pos, s);
+  }
+  if (P.rank == 32) {
+    if (d.order == 3) return launch_planned<W, V, O, 3, 32>(d, P, packed, pos, s);
+    if (d.order == 4) return launch_planned<W, V, O, 4, 32>(d, P, packed, pos, s);
+    if (d.order == 5) return launch_planned<W, V, O, 5, 32>(d, P, packed, pos, s);
   }
   return ALTO_EUNSUPPORTED;
 }

@@ -101,6 +101,8 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   ALTO_REQUIRE((P.hot_copies & (P.hot_copies - 1)) == 0, "hot_copies must be a power of two");
   P.hot_buf = a->hot_buf;
   P.flags = a->flags;
+  P.packed = a->packed;
+  P.pos = a->pos;
   const auto* tab = static_cast<const uint64_t*>(a->d_tables);
   const bool o32 = a->out_dtype == ALTO_F32;
   int st = d.n_words == 1 ? (o32 ? fast_w1_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)

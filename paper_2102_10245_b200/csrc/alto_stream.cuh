@@ -57,7 +57,9 @@ struct StreamParams {
   const int* hot_slot;
   int hot_copies;
   void* hot_buf;  // hot_copies x n_hot x R, element type = output type O
-  int flags;  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
+  int flags;
+  const uint64_t* packed;     // mode-contiguous keys (optional, alto_pack_keys)
+  const unsigned char* pos;   // per-mode sub-tile slots (optional, alto_subtile_order)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
 };
 
 template <typename V, typename F>

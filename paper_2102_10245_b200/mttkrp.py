@@ -111,6 +111,8 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
     a.zero_out = zero_out
     a.n_hot = 0
     a.flags = STREAM_FLAGS
+    a.packed = None
+    a.pos = None
     return a, cl
 
 
@@ -152,8 +154,34 @@ def hot_plan(tensor: AltoTensor, mode: int, rank: int, out_dtype=None):
     return plan
 
 
+def packed_keys(tensor: AltoTensor):
+    """Mode-contiguous re-encoding of the sorted keys (alto_pack_keys), cached."""
+    torch = _torch()
+    hit = tensor._cache.get("packed")
+    if hit is None:
+        lay = tensor.layout
+        hit = torch.empty_like(tensor.keys)
+        _lib.check(_lib.load().alto_pack_keys(c_layout(lay), device_tables(lay).data_ptr(), tensor.keys.data_ptr(),
+                                              tensor.nnz, hit.data_ptr(), _lib.stream_ptr()), "alto_pack_keys")
+        tensor._cache["packed"] = hit
+    return hit
+
+
+def subtile_order(tensor: AltoTensor, mode: int):
+    """Per-mode row-sorted slot of each element in its 128-element sub-tile, cached."""
+    torch = _torch()
+    key = ("pos", mode)
+    hit = tensor._cache.get(key)
+    if hit is None:
+        hit = torch.empty(max(tensor.nnz, 1), dtype=torch.uint8, device=tensor.keys.device)
+        _lib.check(_lib.load().alto_subtile_order(c_layout(tensor.layout), packed_keys(tensor).data_ptr(), tensor.nnz,
+                                                  mode, hit.data_ptr(), _lib.stream_ptr()), "alto_subtile_order")
+        tensor._cache[key] = hit
+    return hit
+
+
 def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int = DEFAULT_TILE,
-                  zero_out: bool = True, hot: bool = True, out_dtype=None):
+                  zero_out: bool = True, hot: bool = True, out_dtype=None, planned: bool = True):
     """Fast streaming ALTO MTTKRP on device tensors -> (I_mode, R) device tensor
     (float64 by default; float32 when requested for float32 data/factors)."""
     torch = _torch()
@@ -164,6 +192,10 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
     if out is None:
         out = torch.empty((dim, rank), dtype=out_dtype or torch.float64, device=tensor.keys.device)
     a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
+    if planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
+            and max(tensor.layout.bits) <= 31:
+        a.packed = packed_keys(tensor).data_ptr()
+        a.pos = subtile_order(tensor, mode).data_ptr()
     hp = hot_plan(tensor, mode, rank, out.dtype) if hot else None
     if hp is not None:
         slot, rows, n, copies, buf = hp

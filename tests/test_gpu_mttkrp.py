@@ -222,6 +222,45 @@ class TestStreamKernel:
             nohot = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, hot=False)
             assert rel_error(nohot.double().cpu().numpy(), ref) <= 1e-5
 
+    @pytest.mark.parametrize("cfg", [2, "wide"])
+    def test_stream_plan(self, at, cfg):
+        """Per-tensor packed keys and per-mode sub-tile order (alto_pack_keys /
+        alto_subtile_order): fields decode to the coordinates; pos is, per
+        128-element sub-tile, the stable row-sorted slot; planned == unplanned."""
+        import torch
+
+        from paper_2102_10245_b200.mttkrp import (factors_to_device, mttkrp_stream, packed_keys,
+                                                  subtile_order)
+
+        st = synth.make_tensor(self.WIDE if cfg == "wide" else cfg, nnz=100_003)
+        dims = st.config.dims
+        alto = at.build_alto(at.CooTensor(dims, st.coords, st.values.astype(np.float64)), dtype="float32")
+        lay = alto.layout
+        coords = orc.decode(orc.build_layout(dims), alto.indices)
+        pk = packed_keys(alto).cpu().numpy().view(np.uint64)
+        ints = [sum(int(w) << (64 * i) for i, w in enumerate(row)) for row in pk[:2000]]
+        off = 0
+        for n in range(len(dims)):
+            got = np.array([(v >> off) & ((1 << lay.bits[n]) - 1) for v in ints])
+            assert np.array_equal(got, coords[:2000, n])
+            off += lay.bits[n]
+        for mode in range(len(dims)):
+            pos = subtile_order(alto, mode).cpu().numpy()[:alto.nnz].astype(np.int64)
+            for s0 in range(0, alto.nnz, 128 * 97):
+                seg = slice(s0, min(s0 + 128, alto.nnz))
+                p, r = pos[seg], coords[seg, mode]
+                assert sorted(p.tolist()) == list(range(len(p)))
+                if r.max() - r.min() < 512:
+                    order = np.argsort(p)
+                    assert (np.diff(r[order]) >= 0).all()
+                    assert np.array_equal(order, np.argsort(r, kind="stable"))
+        rng = np.random.default_rng(4)
+        fdev = factors_to_device([rng.random((d, 16)).astype(np.float32) for d in dims])
+        for mode in range(len(dims)):
+            a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=True).double().cpu().numpy()
+            b = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=False).double().cpu().numpy()
+            assert rel_error(a, b) <= 1e-6
+
     def test_accumulates_into_out(self, at):
         from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
 
