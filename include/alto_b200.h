@@ -171,7 +171,27 @@ typedef struct alto_mttkrp_args {
    * in-tile sort. */
   const uint64_t* packed;
   const uint8_t* pos;
+  /* Plan 2 (preferred over `pos` when set): per-mode 64-bit plan words from
+   * alto_stream_plan and, for up to 3 input modes (mode order, output mode
+   * skipped), the ids of `cache_k` hot rows staged in shared memory. */
+  const uint64_t* plan;
+  const int32_t* cache_rows[3];
+  int32_t cache_k;
+  int32_t cache_modes;
 } alto_mttkrp_args;
+
+/* Top-k rows of a mode by element count (from alto_row_index's row_ptr):
+ * rows (k int32, -1 padded) and slot_map (dim int32: slot or -1). */
+size_t alto_topk_rows_workspace_bytes(int64_t dim);
+int alto_topk_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int32_t* rows, int32_t* slot_map, void* ws,
+                   size_t ws_bytes, void* stream);
+/* Per-mode plan words (see alto_fast.cuh, planned variant 2): slot in the
+ * 256-element sub-tile after a stable counting sort by `mode` coordinate,
+ * hot-input slots for up to 3 input modes (in_slot_maps_host: host array of
+ * `order` device pointers, entries may be NULL) and hot output slot + 1. */
+int alto_stream_plan(const alto_layout* lay, const uint64_t* packed, int64_t m, int32_t mode,
+                     const int32_t* const* in_slot_maps_host, const int32_t* hot_out_slot, uint64_t* plan,
+                     void* stream);
 
 /* Mode-contiguous re-encoding of sorted ALTO keys: packed[i] holds mode n's
  * coordinate in bits [sum_{m<n} b_m, +b_n) (same n_words as the keys). */

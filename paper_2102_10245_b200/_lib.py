@@ -57,6 +57,10 @@ class CMttkrpArgs(Structure):
         ("flags", c_int32),
         ("packed", c_void_p),
         ("pos", c_void_p),
+        ("plan", c_void_p),
+        ("cache_rows", c_void_p * 3),
+        ("cache_k", c_int32),
+        ("cache_modes", c_int32),
     ]
 
 
@@ -84,6 +88,10 @@ SIGNATURES = [
     ("alto_mttkrp", c_int32, [POINTER(CMttkrpArgs), c_void_p]),
     ("alto_pack_keys", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     ("alto_subtile_order", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    ("alto_topk_rows_workspace_bytes", c_size_t, [c_int64]),
+    ("alto_topk_rows", c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("alto_stream_plan", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, POINTER(c_void_p), c_void_p,
+                                   c_void_p, c_void_p]),
     ("alto_hot_plan", c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("alto_row_index_workspace_bytes", c_size_t, [c_int64, c_int64]),
     ("alto_row_index", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,

@@ -139,3 +139,195 @@ int alto_subtile_order(const alto_layout* lay, const uint64_t* packed, int64_t m
 }
 
 }  // extern "C"
+
+// ---- plan 2: per-mode 64-bit plan words and hot-input row selection ----------
+namespace alto {
+
+struct SlotMaps {
+  const int* in_slot[kMaxCacheModes];  // per input mode k (mode order, output mode skipped)
+  const int* hot_out;                   // hot output slot per row (-1 = not hot), or null
+};
+
+template <int W>
+__global__ void stream_plan_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ packed,
+                                   long long m, int mode, const __grid_constant__ SlotMaps S,
+                                   unsigned long long* __restrict__ plan) {
+  __shared__ int s_bins[kTileThreads / 32][kFastBins];
+  constexpr int EPL = kPlanTile / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* bin = s_bins[warp];
+  const long long nsub = (m + kPlanTile - 1) / kPlanTile;
+  const long long nwarps = static_cast<long long>(gridDim.x) * (kTileThreads / 32);
+  const unsigned ltm = (1u << lane) - 1u;
+  const int N = L.order;
+  for (long long sub = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp; sub < nsub; sub += nwarps) {
+    const long long e0 = sub * kPlanTile;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kPlanTile), m - e0));
+    int row[EPL];
+    unsigned long long word[EPL];
+    int lo = INT_MAX, hi = INT_MIN;
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const int e = lane + 32 * k;
+      row[k] = -1;
+      word[k] = 0;
+      if (e < cnt) {
+        const Key<W> key = load_key<W>(packed, e0 + e);
+        unsigned long long w = 0;
+        int q = 0;
+        for (int n = 0; n < N; ++n) {
+          const int c = static_cast<int>(packed_field32<W>(key, L.pack_off[n], L.bits[n]));
+          if (n == mode) {
+            row[k] = c;
+            if (S.hot_out) {
+              const int hs = S.hot_out[c];
+              if (hs >= 0) w |= static_cast<unsigned long long>((hs + 1) & 0xffff) << 32;
+            }
+          } else {
+            unsigned h = 0xffu;
+            if (q < kMaxCacheModes && S.in_slot[q]) {
+              const int sl = S.in_slot[q][c];
+              if (sl >= 0 && sl < 255) h = static_cast<unsigned>(sl);
+            }
+            if (q < kMaxCacheModes) w |= static_cast<unsigned long long>(h) << (8 + 8 * q);
+            ++q;
+          }
+        }
+        word[k] = w;
+        lo = min(lo, row[k]);
+        hi = max(hi, row[k]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int span = hi - lo + 1;
+    if (span > kFastBins) {
+#pragma unroll
+      for (int k = 0; k < EPL; ++k)
+        if (row[k] >= 0) plan[e0 + lane + 32 * k] = word[k] | static_cast<unsigned long long>(lane + 32 * k);
+      continue;
+    }
+    for (int i = lane; i < span; i += 32) bin[i] = 0;
+    __syncwarp();
+    unsigned peers[EPL];
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const bool ok = row[k] >= 0;
+      peers[k] = __match_any_sync(0xffffffffu, ok ? row[k] : -1 - lane);
+      if (ok && (peers[k] & ltm) == 0) bin[row[k] - lo] += __popc(peers[k]);
+      __syncwarp();
+    }
+    int carry = 0;
+    for (int base = 0; base < span; base += 32) {
+      const int i = base + lane;
+      const int v = i < span ? bin[i] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < span) bin[i] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const bool ok = row[k] >= 0;
+      const int leader = __ffs(peers[k]) - 1;
+      int b = 0;
+      if (ok && leader == lane) {
+        b = bin[row[k] - lo];
+        bin[row[k] - lo] = b + __popc(peers[k]);
+      }
+      b = __shfl_sync(0xffffffffu, b, leader);
+      if (ok) plan[e0 + lane + 32 * k] = word[k] | static_cast<unsigned long long>(b + __popc(peers[k] & ltm));
+      __syncwarp();
+    }
+  }
+}
+
+// keys[r] = (count << 32) | (0xffffffff - r) so an ascending sort puts the
+// highest counts last (ties: lower row first).
+__global__ void topk_keys_kernel(const long long* __restrict__ row_ptr, long long dim, uint64_t* __restrict__ keys) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < dim; r += stride) {
+    const unsigned long long c = static_cast<unsigned long long>(row_ptr[r + 1] - row_ptr[r]);
+    keys[r] = (min(c, 0xffffffffull) << 32) | (0xffffffffull - static_cast<unsigned long long>(r));
+  }
+}
+
+__global__ void topk_finish_kernel(const uint64_t* __restrict__ sorted, long long dim, int k, int* __restrict__ rows,
+                                   int* __restrict__ slot_map) {
+  for (int s = threadIdx.x; s < k; s += blockDim.x) {
+    const long long idx = dim - 1 - s;
+    int r = -1;
+    if (idx >= 0 && (sorted[idx] >> 32) > 0) r = static_cast<int>(0xffffffffull - (sorted[idx] & 0xffffffffull));
+    rows[s] = r;
+    if (r >= 0) slot_map[r] = s;
+  }
+}
+
+__global__ void fill_i32(int* p, long long n, int v) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride) p[i] = v;
+}
+
+}  // namespace alto
+
+extern "C" {
+
+size_t alto_topk_rows_workspace_bytes(int64_t dim) {
+  if (dim < 1) dim = 1;
+  return ((static_cast<size_t>(dim) * 8 + 255) & ~size_t(255)) + alto_sort_workspace_bytes(dim, 1, 0);
+}
+
+int alto_topk_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int32_t* rows, int32_t* slot_map, void* ws,
+                   size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(dim >= 1 && dim <= INT_MAX, "topk needs 1 <= dim < 2^31");
+  ALTO_REQUIRE(k >= 1 && k <= 255, "topk k must be in [1, 255]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_topk_rows_workspace_bytes(dim), "topk workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* keys = static_cast<uint64_t*>(ws);
+  const size_t a = (static_cast<size_t>(dim) * 8 + 255) & ~size_t(255);
+  topk_keys_kernel<<<grid_for(dim, 256), 256, 0, s>>>(reinterpret_cast<const long long*>(row_ptr), dim, keys);
+  fill_i32<<<grid_for(dim, 256), 256, 0, s>>>(slot_map, dim, -1);
+  ALTO_LAUNCH_CHECK("alto_topk_rows");
+  const int st = alto_sort_pairs(keys, nullptr, dim, 1, 0, 64, static_cast<char*>(ws) + a, ws_bytes - a, stream);
+  if (st) return st;
+  topk_finish_kernel<<<1, 256, 0, s>>>(keys, dim, k, rows, slot_map);
+  ALTO_LAUNCH_CHECK("alto_topk_rows/finish");
+  return ALTO_OK;
+}
+
+int alto_stream_plan(const alto_layout* lay, const uint64_t* packed, int64_t m, int32_t mode,
+                     const int32_t* const* in_slot_maps_host, const int32_t* hot_out_slot, uint64_t* plan,
+                     void* stream) {
+  ALTO_REQUIRE(lay && mode >= 0 && mode < lay->order, "mode out of range");
+  for (int n = 0; n < lay->order; ++n) ALTO_REQUIRE(lay->bits[n] <= 31, "stream plan needs extents below 2^31");
+  if (m <= 0) return ALTO_OK;
+  const DevLayout d = make_dev_layout(lay);
+  SlotMaps S{};
+  int q = 0;
+  for (int n = 0; n < lay->order; ++n) {
+    if (n == mode) continue;
+    if (q < kMaxCacheModes) S.in_slot[q] = in_slot_maps_host ? in_slot_maps_host[n] : nullptr;
+    ++q;
+  }
+  S.hot_out = hot_out_slot;
+  cudaStream_t s = as_stream(stream);
+  const long long nsub = (m + kPlanTile - 1) / kPlanTile;
+  const int grid = grid_for(nsub, kTileThreads / 32, kSMs * 8);
+  auto* pl = reinterpret_cast<unsigned long long*>(plan);
+  if (d.n_words == 1)
+    stream_plan_kernel<1><<<grid, kTileThreads, 0, s>>>(d, packed, m, mode, S, pl);
+  else
+    stream_plan_kernel<2><<<grid, kTileThreads, 0, s>>>(d, packed, m, mode, S, pl);
+  ALTO_LAUNCH_CHECK("alto_stream_plan");
+  return ALTO_OK;
+}
+
+}  // extern "C"

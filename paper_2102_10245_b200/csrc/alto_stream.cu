@@ -1,6 +1,6 @@
 // alto_stream.cu — C ABI of the streaming ALTO MTTKRP (see alto_stream.cuh
 // for the kernel design), the hot-row plan and the hot-copy reduction.
-#include "alto_stream.cuh"
+#include "alto_fast.cuh"
 
 namespace alto {
 
@@ -103,6 +103,17 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.flags = a->flags;
   P.packed = a->packed;
   P.pos = a->pos;
+  Plan2 pl2{};
+  P.plan2 = nullptr;
+  if (a->plan) {
+    pl2.plan = reinterpret_cast<const unsigned long long*>(a->plan);
+    for (int k = 0; k < kMaxCacheModes; ++k) pl2.cache_rows[k] = a->cache_rows[k];
+    pl2.cache_k = a->cache_k;
+    pl2.cache_modes = a->cache_k > 0 ? std::min(a->cache_modes, kMaxCacheModes) : 0;
+    for (int k = 0; k < pl2.cache_modes; ++k) ALTO_REQUIRE(pl2.cache_rows[k] != nullptr, "cache rows missing");
+    ALTO_REQUIRE(pl2.cache_k >= 0 && pl2.cache_k <= 255, "cache_k must be in [0, 255]");
+    P.plan2 = &pl2;
+  }
   const auto* tab = static_cast<const uint64_t*>(a->d_tables);
   const bool o32 = a->out_dtype == ALTO_F32;
   int st = d.n_words == 1 ? (o32 ? fast_w1_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)

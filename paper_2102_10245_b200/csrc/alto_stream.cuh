@@ -43,6 +43,7 @@ constexpr int kSortBins = 2048;
 constexpr int kEPT = 4;  // elements per thread in phase A -> tile <= 1024
 constexpr int kRecPad = 4 * kTileThreads;  // words of swizzle headroom (4 per phase-B chunk)
 
+struct Plan2;
 struct StreamParams {
   const uint64_t* keys;
   const void* values;
@@ -59,7 +60,8 @@ struct StreamParams {
   void* hot_buf;  // hot_copies x n_hot x R, element type = output type O
   int flags;
   const uint64_t* packed;     // mode-contiguous keys (optional, alto_pack_keys)
-  const unsigned char* pos;   // per-mode sub-tile slots (optional, alto_subtile_order)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
+  const unsigned char* pos;   // per-mode sub-tile slots (optional, alto_subtile_order)
+  const Plan2* plan2;         // per-mode plan words + hot-input caches (optional, host struct)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
 };
 
 template <typename V, typename F>

@@ -113,6 +113,9 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
     a.flags = STREAM_FLAGS
     a.packed = None
     a.pos = None
+    a.plan = None
+    a.cache_k = 0
+    a.cache_modes = 0
     return a, cl
 
 
@@ -125,33 +128,103 @@ HOT_MAX = 8192
 HOT_COPIES = {4: 128, 8: 32}
 
 
+def hot_slots(tensor: AltoTensor, mode: int):
+    """Per-mode hot-row slots (rows with more than HOT_TAU elements), cached:
+    (slot map (I_mode,) int32, hot row ids, count) or None."""
+    torch = _torch()
+    key = ("hotslots", mode)
+    if key in tensor._cache:
+        return tensor._cache[key]
+    res = None
+    if tensor.nnz > HOT_TAU:
+        lib = _lib.load()
+        dim = tensor.layout.dims[mode]
+        dev = tensor.keys.device
+        _perm, ptr = row_index(tensor, mode)
+        slot = torch.empty(dim, dtype=torch.int32, device=dev)
+        rows = torch.empty(HOT_MAX, dtype=torch.int32, device=dev)
+        nhot = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.check(lib.alto_hot_plan(ptr.data_ptr(), dim, HOT_TAU, HOT_MAX, slot.data_ptr(), rows.data_ptr(),
+                                     nhot.data_ptr(), _lib.stream_ptr()), "alto_hot_plan")
+        n = int(nhot.item())
+        if n > 0:
+            res = (slot, rows, n)
+    tensor._cache[key] = res
+    return res
+
+
 def hot_plan(tensor: AltoTensor, mode: int, rank: int, out_dtype=None):
-    """Per-(mode, rank, output dtype) hot-row plan, built once from the row index and cached."""
+    """Hot-row plan of one mode with zeroed replicated copies for (rank, output dtype), cached."""
     torch = _torch()
     out_dtype = out_dtype or torch.float64
     key = ("hot", mode, rank, out_dtype)
     if key in tensor._cache:
         return tensor._cache[key]
-    lib = _lib.load()
-    dim = tensor.layout.dims[mode]
-    dev = tensor.keys.device
-    if tensor.nnz <= HOT_TAU:
-        tensor._cache[key] = None
-        return None
-    _perm, ptr = row_index(tensor, mode)
-    slot = torch.empty(dim, dtype=torch.int32, device=dev)
-    rows = torch.empty(HOT_MAX, dtype=torch.int32, device=dev)
-    nhot = torch.zeros(1, dtype=torch.int32, device=dev)
-    _lib.check(lib.alto_hot_plan(ptr.data_ptr(), dim, HOT_TAU, HOT_MAX, slot.data_ptr(), rows.data_ptr(),
-                                 nhot.data_ptr(), _lib.stream_ptr()), "alto_hot_plan")
-    n = int(nhot.item())
+    hs = hot_slots(tensor, mode)
     plan = None
-    if n > 0:
+    if hs is not None:
+        slot, rows, n = hs
         copies = HOT_COPIES[torch.empty(0, dtype=out_dtype).element_size()]
-        buf = torch.zeros(copies * n * rank, dtype=out_dtype, device=dev)
+        buf = torch.zeros(copies * n * rank, dtype=out_dtype, device=tensor.keys.device)
         plan = (slot, rows, n, copies, buf)
     tensor._cache[key] = plan
     return plan
+
+
+# Shared-memory budget (bytes per CTA) for the hot-input row cache.
+CACHE_BUDGET = int(__import__("os").environ.get("ALTO_CACHE_BUDGET", 32 * 1024))
+# Default planned variant: "plan2" (plan words + hot-input cache) or "pos".
+PLAN_VARIANT = __import__("os").environ.get("ALTO_PLAN", "pos")
+
+
+def topk_rows(tensor: AltoTensor, mode: int, k: int):
+    """The k rows of `mode` with the most elements: (rows (k,) int32, slot map (I,) int32), cached."""
+    torch = _torch()
+    key = ("topk", mode, k)
+    hit = tensor._cache.get(key)
+    if hit is None:
+        lib = _lib.load()
+        dim = tensor.layout.dims[mode]
+        dev = tensor.keys.device
+        _perm, ptr = row_index(tensor, mode)
+        rows = torch.empty(k, dtype=torch.int32, device=dev)
+        smap = torch.empty(dim, dtype=torch.int32, device=dev)
+        wsb = lib.alto_topk_rows_workspace_bytes(dim)
+        ws = torch.empty(int(wsb), dtype=torch.uint8, device=dev)
+        _lib.check(lib.alto_topk_rows(ptr.data_ptr(), dim, k, rows.data_ptr(), smap.data_ptr(), ws.data_ptr(), wsb,
+                                      _lib.stream_ptr()), "alto_topk_rows")
+        hit = (rows, smap)
+        tensor._cache[key] = hit
+    return hit
+
+
+def stream_plan(tensor: AltoTensor, mode: int, rank: int, fbytes: int):
+    """Per-mode plan words (alto_stream_plan) + hot-input row caches, cached."""
+    torch = _torch()
+    order = tensor.layout.order
+    n_cache = min(order - 1, 3)
+    k = max(0, min(255, CACHE_BUDGET // max(1, n_cache * rank * fbytes)))
+    key = ("plan2", mode, k)
+    hit = tensor._cache.get(key)
+    if hit is not None:
+        return hit
+    lib = _lib.load()
+    in_modes = [n for n in range(order) if n != mode][:n_cache]
+    cache_rows, smaps = [], [None] * order
+    if k > 0:
+        for n in in_modes:
+            rows, smap = topk_rows(tensor, n, k)
+            cache_rows.append(rows)
+            smaps[n] = smap
+    hs = hot_slots(tensor, mode)
+    plan = torch.empty(max(tensor.nnz, 1), dtype=torch.int64, device=tensor.keys.device)
+    arr = (ctypes.c_void_p * order)(*[None if sm is None else sm.data_ptr() for sm in smaps])
+    _lib.check(lib.alto_stream_plan(c_layout(tensor.layout), packed_keys(tensor).data_ptr(), tensor.nnz, mode, arr,
+                                    None if hs is None else hs[0].data_ptr(), plan.data_ptr(), _lib.stream_ptr()),
+               "alto_stream_plan")
+    hit = {"plan": plan, "cache_rows": cache_rows, "k": k if cache_rows else 0, "modes": len(cache_rows)}
+    tensor._cache[key] = hit
+    return hit
 
 
 def packed_keys(tensor: AltoTensor):
@@ -195,7 +268,15 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
     if planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
             and max(tensor.layout.bits) <= 31:
         a.packed = packed_keys(tensor).data_ptr()
-        a.pos = subtile_order(tensor, mode).data_ptr()
+        if planned == "pos" or (planned is True and PLAN_VARIANT == "pos"):
+            a.pos = subtile_order(tensor, mode).data_ptr()
+        else:
+            sp = stream_plan(tensor, mode, rank, fdev[0].element_size())
+            a.plan = sp["plan"].data_ptr()
+            for i, rws in enumerate(sp["cache_rows"]):
+                a.cache_rows[i] = rws.data_ptr()
+            a.cache_k = sp["k"]
+            a.cache_modes = sp["modes"]
     hp = hot_plan(tensor, mode, rank, out.dtype) if hot else None
     if hp is not None:
         slot, rows, n, copies, buf = hp

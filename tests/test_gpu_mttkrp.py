@@ -257,9 +257,10 @@ class TestStreamKernel:
         rng = np.random.default_rng(4)
         fdev = factors_to_device([rng.random((d, 16)).astype(np.float32) for d in dims])
         for mode in range(len(dims)):
-            a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=True).double().cpu().numpy()
             b = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=False).double().cpu().numpy()
-            assert rel_error(a, b) <= 1e-6
+            for variant in (True, "pos"):
+                a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=variant).double().cpu().numpy()
+                assert rel_error(a, b) <= 1e-6, variant
 
     def test_accumulates_into_out(self, at):
         from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
