@@ -213,15 +213,19 @@ def run_b200(args):
     cfg = synth.CONFIGS[args.config]
     nnz_total = args.nnz or cfg.nnz
     t_gen = time.time()
-    st = synth.make_tensor(args.config, nnz=nnz_total)
+    vdt = torch.float32 if cfg.value_dtype == "float32" else torch.float64
+    if args.gen == "host":
+        st = synth.make_tensor(args.config, nnz=nnz_total)
+        coords = torch.from_numpy(st.coords).to(dev)
+        vals = torch.from_numpy(st.values).to(device=dev, dtype=vdt)
+    else:
+        coords, vals = synth.make_tensor_device(args.config, nnz=nnz_total, device=dev)
+    torch.cuda.synchronize()
     t_gen = time.time() - t_gen
     dims = cfg.dims
     R = cfg.rank
     lay = build_masks(dims)
     # ALTO build on device (whole tensor), then keep this rank's key-range shard
-    coords = torch.from_numpy(st.coords).to(dev)
-    vdt = torch.float32 if cfg.value_dtype == "float32" else torch.float64
-    vals = torch.from_numpy(st.values).to(device=dev, dtype=vdt)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -374,7 +378,7 @@ def run_b200(args):
             "metric": "MTTKRP nonzeros/sec (mode-averaged)",
             "value": value, "unit": "nnz/s", "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; BASELINE.json cfg2 law)",
+            "vs_baseline": None, "dtype": "f32", "data": f"synthetic (seeded; BASELINE.json {cfg.name} law; generated on {args.gen})",
             "config": {"workload": f"{cfg.name}: {'x'.join(map(str, dims))}, {nnz_total} nnz, Zipf(1.1) all modes, "
                                    f"fp32 values, rank {R}; step = MTTKRP all {N} modes",
                        "nnz": nnz_total, "rank": R, "tile": args.tile, "key_bits": lay.total_bits,
@@ -417,6 +421,8 @@ def main():
     ap.add_argument("--skip-cpals", action="store_true")
     ap.add_argument("--no-hot", action="store_true", help="disable the hot-row plan (A/B)")
     ap.add_argument("--out", default="f32", choices=["f32", "f64"], help="MTTKRP output dtype of the bench step")
+    ap.add_argument("--gen", default="device", choices=["device", "host"],
+                    help="synthetic input generator: torch on the GPU (fast) or the NumPy stream of the parity tests")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

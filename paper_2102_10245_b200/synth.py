@@ -170,3 +170,76 @@ def make_factors(dims, rank: int, dtype="float64", seed: int = 0) -> list[np.nda
     """MTTKRP factors: default_rng(seed).random((I_n, R)) per mode, in order."""
     rng = np.random.default_rng(seed)
     return [rng.random((int(d), rank)).astype(dtype) for d in dims]
+
+
+def make_tensor_device(cfg: int | SynthConfig, nnz: int | None = None, seed: int | None = None, device="cuda"):
+    """Same laws as make_tensor, drawn on the GPU with torch's generator (fast
+    benchmark inputs; not bit-identical to the NumPy stream).  Distinct
+    coordinate tuples are obtained by drawing, deduplicating with
+    torch.unique and keeping a uniformly random subset of exactly `nnz`.
+    Returns (coords (nnz, N) int64, values (nnz,) value_dtype) on `device`."""
+    import torch
+
+    c = CONFIGS[cfg] if isinstance(cfg, int) else cfg
+    m = c.nnz if nnz is None else int(nnz)
+    sd = (SEED_TENSOR_BASE + int(c.name[3:])) if seed is None else seed
+    g = torch.Generator(device=device)
+    g.manual_seed(sd)
+    bits = [max((int(d) - 1).bit_length(), 0) for d in c.dims]
+    cdfs = []
+    for d, (law, s) in zip(c.dims, c.laws):
+        if law == "zipf":
+            w = torch.arange(1, int(d) + 1, dtype=torch.float64, device=device).pow_(-s)
+            w = torch.cumsum(w, 0)
+            cdfs.append(w / w[-1])
+        else:
+            cdfs.append(None)
+
+    def draw(k):
+        cols = []
+        for n, d in enumerate(c.dims):
+            if cdfs[n] is None:
+                cols.append(torch.randint(0, int(d), (k,), generator=g, device=device, dtype=torch.int64))
+            else:
+                u = torch.rand(k, generator=g, device=device, dtype=torch.float64)
+                cols.append(torch.clamp(torch.searchsorted(cdfs[n], u, right=True), max=int(d) - 1))
+        return torch.stack(cols, 1)
+
+    def pack(x):
+        # two int64 words (mixed radix), exact for <= 124 total bits
+        hi = torch.zeros(x.shape[0], dtype=torch.int64, device=device)
+        lo = torch.zeros_like(hi)
+        used = 0
+        for n, b in enumerate(bits):
+            if used + b <= 62:
+                lo |= x[:, n] << used
+            else:
+                hi = (hi << b) | x[:, n]
+            used += b
+        return hi, lo
+
+    have = None
+    factor = 1.1
+    while True:
+        need = m - (0 if have is None else have.shape[0])
+        batch = draw(max(int(need * factor), 1024))
+        allc = batch if have is None else torch.cat([have, batch])
+        hi, lo = pack(allc)
+        key = torch.stack([hi, lo], 1)
+        _, inv = torch.unique(key, dim=0, return_inverse=True)
+        first = torch.full((int(inv.max()) + 1,), allc.shape[0], dtype=torch.int64, device=device)
+        first.scatter_reduce_(0, inv, torch.arange(allc.shape[0], device=device), reduce="amin")
+        have = allc[first]
+        del allc, key, inv, hi, lo
+        if have.shape[0] >= m:
+            sel = torch.randperm(have.shape[0], generator=g, device=device)[:m]
+            coords = have[sel].contiguous()
+            break
+        factor = min(factor * 1.5, 4.0)
+    if c.values == "uniform01":
+        vals = torch.rand(m, generator=g, device=device, dtype=torch.float64)
+    elif c.values == "lognormal":
+        vals = torch.exp(torch.randn(m, generator=g, device=device, dtype=torch.float64))
+    else:
+        vals = torch.rand(m, generator=g, device=device, dtype=torch.float64) * 2.0 - 1.0
+    return coords, vals.to(torch.float32 if c.value_dtype == "float32" else torch.float64)

@@ -258,7 +258,7 @@ class TestStreamKernel:
         fdev = factors_to_device([rng.random((d, 16)).astype(np.float32) for d in dims])
         for mode in range(len(dims)):
             b = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=False).double().cpu().numpy()
-            for variant in (True, "pos"):
+            for variant in (True, "pos", "plan2"):
                 a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=variant).double().cpu().numpy()
                 assert rel_error(a, b) <= 1e-6, variant
 
