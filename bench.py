@@ -316,7 +316,7 @@ def run_b200(args):
     achieved = tot_b / tot_t / 1e9
     traffic, traffic_src = None, None
     if ws == 1 and nnz_total == cfg.nnz and args.config == 2 and args.out == "f32" and not args.no_hot:
-        traffic, traffic_src = traffic_from_profile("stream_kernel<1, float, float, float, 3, 4")
+        traffic, traffic_src = traffic_from_profile("planned_kernel<1, float, float, 3, 16")
 
     # end-to-end through the reference-facing API: mttkrp_par with an Atomic plan
     # (the CLI protocol: prepare once, cli.py:194; per step host factors in,
@@ -390,7 +390,7 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "traffic": traffic, "traffic_source": traffic_src,
-                         "bytes_alg_per_launch": tot_b / N, "kernel": "alto::stream_kernel (alto_stream.cuh)",
+                         "bytes_alg_per_launch": tot_b / N, "kernel": "alto::planned_kernel (alto_fast.cuh)",
                          "per_mode": per_mode},
             "e2e": {"value": N * nnz_total / (e2e_ms * 1e-3), "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,

@@ -4,34 +4,46 @@
 
 namespace alto {
 
-// Sum the replicated hot-row partials in copy order into out; re-zero them.
-// One thread per (hot row, rank) element; the copy loop is unrolled so 16
-// independent loads are in flight per thread (the copies live in L2).
+// Sum the replicated hot-row partials into out and re-zero them.  A block
+// covers 32 (hot row, rank) elements x 8 copy groups: thread (g, lane) sums
+// copies g, g+8, ... of its element (coalesced across lanes), then group 0
+// adds the 8 partials in a fixed order (deterministic).
 template <typename O>
 __global__ void __launch_bounds__(256) hot_reduce_kernel(O* __restrict__ buf, const int* __restrict__ hot_rows,
                                                          int n_hot, int copies, int R, O* __restrict__ out) {
+  __shared__ double s_part[8][33];
   const long long n = static_cast<long long>(n_hot) * R;
-  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const long long i = static_cast<long long>(blockIdx.x) * 32 + lane;
   double s = 0.0;
-  int k = 0;
-  for (; k + 16 <= copies; k += 16) {
-    O v[16];
+  if (i < n) {
+    // loads first, then the zeroing stores (no load-after-store chains)
+    constexpr int B = 8;
+    for (int k0 = g; k0 < copies; k0 += 8 * B) {
+      O v[B];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = buf[(k + u) * n + i];
+      for (int u = 0; u < B; ++u) {
+        const int k = k0 + 8 * u;
+        v[u] = k < copies ? buf[k * n + i] : O(0);
+      }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      s += static_cast<double>(v[u]);
-      buf[(k + u) * n + i] = O(0);
+      for (int u = 0; u < B; ++u) {
+        const int k = k0 + 8 * u;
+        s += static_cast<double>(v[u]);
+        if (k < copies) buf[k * n + i] = O(0);
+      }
     }
   }
-  for (; k < copies; ++k) {
-    s += static_cast<double>(buf[k * n + i]);
-    buf[k * n + i] = O(0);
+  s_part[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && i < n) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += s_part[q][lane];
+    const long long h = i / R;
+    O* o = out + static_cast<long long>(hot_rows[h]) * R + (i - h * R);
+    *o = static_cast<O>(static_cast<double>(*o) + t);
   }
-  const long long h = i / R;
-  O* o = out + static_cast<long long>(hot_rows[h]) * R + (i - h * R);
-  *o = static_cast<O>(static_cast<double>(*o) + s);
 }
 
 __global__ void hot_plan_kernel(const long long* __restrict__ row_ptr, long long dim, long long tau, int hmax,
@@ -128,7 +140,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   if (st) return st;
   if (P.n_hot > 0) {
     const long long nh = static_cast<long long>(P.n_hot) * a->rank;
-    const int grid = static_cast<int>((nh + 255) / 256);
+    const int grid = static_cast<int>((nh + 31) / 32);
     if (a->out_dtype == ALTO_F32)
       hot_reduce_kernel<float><<<grid, 256, 0, s>>>(static_cast<float*>(P.hot_buf), a->hot_rows, P.n_hot, P.hot_copies, a->rank,
                                                      static_cast<float*>(a->out));

@@ -125,7 +125,7 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
 HOT_TAU = 1024
 HOT_MAX = 8192
 # float32 copies take fewer adds each (precision); float64 copies fewer bytes
-HOT_COPIES = {4: 128, 8: 32}
+HOT_COPIES = {4: 64, 8: 32}
 
 
 def hot_slots(tensor: AltoTensor, mode: int):

@@ -19,6 +19,9 @@ import subprocess
 import sys
 
 
+STEP_KERNELS = ("planned_kernel<1, float, float, 3, 16", "hot_reduce_kernel<float>")
+
+
 def launches(path: str, out: str) -> None:
     rows = [r for r in csv.reader(open(path)) if len(r) > 10 and r[0] != "ID"]
     tot = collections.defaultdict(float)
@@ -31,6 +34,13 @@ def launches(path: str, out: str) -> None:
     lines = ["| kernel | launches | total us | share |", "|---|---|---|---|"]
     for name, t in sorted(tot.items(), key=lambda kv: -kv[1]):
         lines.append(f"| `{name}` | {cnt[name]} | {t:.1f} | {t / grand * 100:.1f}% |")
+    step = {n: t for n, t in tot.items() if any(k in n for k in STEP_KERNELS)}
+    st = sum(step.values()) or 1.0
+    lines += ["", "Kernels of the timed bench step (f32 output; the process above also "
+              "generates inputs, builds the tensor and runs the e2e/fp64 API leg):", "",
+              "| kernel | share of step |", "|---|---|"]
+    for name, t in sorted(step.items(), key=lambda kv: -kv[1]):
+        lines.append(f"| `{name}` | {t / st * 100:.1f}% |")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
