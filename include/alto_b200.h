@@ -312,6 +312,7 @@ int alto_unpack_rows(void* dst, int32_t dtype, const int64_t* rows, int64_t n, i
                      void* stream);
 /* Cast helpers for factor uploads: out32[i] = (float)in64[i]. */
 int alto_cast_f64_f32(const double* in, float* out, int64_t n, void* stream);
+int alto_cast_f32_f64(const float* in, double* out, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

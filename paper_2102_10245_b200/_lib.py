@@ -108,6 +108,7 @@ SIGNATURES = [
                                  c_size_t, c_void_p]),
     ("alto_sumsq", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_cast_f64_f32", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+    ("alto_cast_f32_f64", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
     ("alto_pack_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_unpack_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_gram_masked", c_int32, [c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t,

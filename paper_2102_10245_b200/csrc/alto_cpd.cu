@@ -522,3 +522,18 @@ int alto_fit_inner_masked(const double* mttkrp, const double* f, const double* l
 }
 
 }  // extern "C"
+
+namespace alto {
+__global__ void cast_f32_f64_kernel(const float* __restrict__ in, double* __restrict__ out, long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    out[i] = static_cast<double>(in[i]);
+}
+}  // namespace alto
+
+extern "C" int alto_cast_f32_f64(const float* in, double* out, int64_t n, void* stream) {
+  if (n <= 0) return ALTO_OK;
+  alto::cast_f32_f64_kernel<<<alto::grid_for(n, 256), 256, 0, alto::as_stream(stream)>>>(in, out, n);
+  ALTO_LAUNCH_CHECK("alto_cast_f32_f64");
+  return ALTO_OK;
+}

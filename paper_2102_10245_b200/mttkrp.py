@@ -32,6 +32,8 @@ from .layout import c_layout, device_tables
 CHUNK = 1 << 17
 # Elements per CTA tile of the streaming kernel.
 DEFAULT_TILE = 1024
+# float32 data with a float64 result: merge in float32 and upcast once.
+F32_ACCUMULATE = __import__("os").environ.get("ALTO_F32_ACCUMULATE", "1") == "1"
 # Streaming-kernel tuning switches (ALTO_STREAM_* in include/alto_b200.h).
 STREAM_FLAGS = int(__import__("os").environ.get("ALTO_STREAM_FLAGS", "0"))
 
@@ -264,6 +266,20 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
         fdev = [f.double() for f in fdev]  # exact upcast; the kernel pairs f64 values with f64 factors
     if out is None:
         out = torch.empty((dim, rank), dtype=out_dtype or torch.float64, device=tensor.keys.device)
+    if (out.dtype == torch.float64 and tensor.vals.dtype == torch.float32 and fdev[0].dtype == torch.float32
+            and F32_ACCUMULATE):
+        # float32 data: accumulate with float32 merges (RED.F32x4; hot rows
+        # still summed in float64 across copies), then upcast the result
+        tmp = mttkrp_stream(tensor, fdev, mode, None, tile, True, hot, torch.float32, planned)
+        if not zero_out:
+            tmp64 = torch.empty_like(out)
+            _lib.check(_lib.load().alto_cast_f32_f64(tmp.data_ptr(), tmp64.data_ptr(), tmp.numel(),
+                                                     _lib.stream_ptr()), "alto_cast_f32_f64")
+            out += tmp64
+        else:
+            _lib.check(_lib.load().alto_cast_f32_f64(tmp.data_ptr(), out.data_ptr(), tmp.numel(),
+                                                     _lib.stream_ptr()), "alto_cast_f32_f64")
+        return out
     a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
     if planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
             and max(tensor.layout.bits) <= 31:
