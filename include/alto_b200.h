@@ -44,7 +44,7 @@ enum alto_status {
   ALTO_ESINGULAR = 5   /* normal equations singular -> np.linalg.LinAlgError */
 };
 
-enum alto_dtype { ALTO_F32 = 0, ALTO_F64 = 1 };
+enum alto_dtype { ALTO_F32 = 0, ALTO_F64 = 1, ALTO_I64 = 2 /* fixed-point MTTKRP output */ };
 
 /* Bit layout of the linearized index (pkg/src/altotensor/layout.py:38-71).
  * Filled on the host from AltoLayout.positions; pos[n][g] is the key bit
@@ -145,7 +145,9 @@ typedef struct alto_mttkrp_args {
   int32_t factor_dtype;          /* ALTO_F32 / ALTO_F64 */
   const void* factors[ALTO_MAX_ORDER]; /* (I_n, rank) row-major, factor_dtype */
   void* out;                     /* (I_mode, rank) row-major, out_dtype     */
-  int32_t out_dtype;             /* ALTO_F64 (reference dtype) or ALTO_F32
+  int32_t out_dtype;             /* ALTO_F64 (reference dtype), ALTO_F32, or
+                                    ALTO_I64: deterministic fixed point,
+                                    out = round(value * *fixed_scale)
                                     (streaming kernel only)                 */
   int32_t tile;                  /* elements per tile (multiple of 256, <= 1024) */
   int32_t zero_out;              /* 1: out is zeroed first (stream-ordered) */
@@ -178,7 +180,20 @@ typedef struct alto_mttkrp_args {
   const int32_t* cache_rows[3];
   int32_t cache_k;
   int32_t cache_modes;
+  const double* fixed_scale;     /* device scalar for ALTO_I64 output (alto_fixed_scale) */
 } alto_mttkrp_args;
+
+/* Deterministic MTTKRP support (ALTO_I64 output).  alto_sumabs / alto_absmax:
+ * float64 sum of |x| / max |x| (fixed-order two-stage reductions, `ws` from
+ * alto_cpd_workspace_bytes).  alto_fixed_scale: scale = 2^(61 - ceil(log2 B))
+ * for B = product of the nterms device scalars (a bound on every partial
+ * sum: sum|v| * prod max|F|), so int64 partial sums cannot overflow.
+ * alto_fixed_to_float: out = in / scale as float32 or float64. */
+int alto_sumabs(const void* x, int32_t dtype, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream);
+int alto_absmax(const void* x, int32_t dtype, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream);
+int alto_fixed_scale(const double* terms, int32_t nterms, double* scale, void* stream);
+int alto_fixed_to_float(const int64_t* in, const double* scale, void* out, int32_t out_dtype, int64_t n,
+                        void* stream);
 
 /* Top-k rows of a mode by element count (from alto_row_index's row_ptr):
  * rows (k int32, -1 padded) and slot_map (dim int32: slot or -1). */

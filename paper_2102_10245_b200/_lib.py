@@ -16,7 +16,7 @@ import numpy as np
 
 ALTO_MAX_ORDER = 8
 ALTO_OK, ALTO_EINVAL, ALTO_ECUDA, ALTO_EUNSUPPORTED, ALTO_ENCCL, ALTO_ESINGULAR = range(6)
-ALTO_F32, ALTO_F64 = 0, 1
+ALTO_F32, ALTO_F64, ALTO_I64 = 0, 1, 2
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libalto_b200.so")
 
@@ -61,6 +61,7 @@ class CMttkrpArgs(Structure):
         ("cache_rows", c_void_p * 3),
         ("cache_k", c_int32),
         ("cache_modes", c_int32),
+        ("fixed_scale", c_void_p),
     ]
 
 
@@ -109,6 +110,10 @@ SIGNATURES = [
     ("alto_sumsq", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_cast_f64_f32", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
     ("alto_cast_f32_f64", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+    ("alto_sumabs", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("alto_absmax", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("alto_fixed_scale", c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),
+    ("alto_fixed_to_float", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p]),
     ("alto_pack_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_unpack_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_gram_masked", c_int32, [c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t,

@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 from .format import (AltoTensor, Strategy, apply_boundary_flags, partition,
                      plan_conflicts)
-from .mttkrp import (_check_factors, factors_to_device, mttkrp_exact,
+from .mttkrp import (_check_factors, factors_to_device, mttkrp_deterministic,
                      mttkrp_seq, mttkrp_stream)
 
 BACKENDS = ("seq", "oracle", "auto", "buffered", "atomic")
@@ -226,7 +226,7 @@ class DeviceBackend:
             return mttkrp_stream(self.tensor, fdev, mode, out=out)
         if eng == "coo":
             return _coo_run(self.tensor, fdev, mode)
-        return mttkrp_exact(self.tensor, fdev, mode, self.offsets[mode], out=out)
+        return mttkrp_deterministic(self.tensor, fdev, mode, self.offsets[mode], out=out)
 
 
 def _coo_run(tensor: AltoTensor, fdev: list, mode: int):

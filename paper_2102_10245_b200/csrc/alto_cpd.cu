@@ -537,3 +537,98 @@ extern "C" int alto_cast_f32_f64(const float* in, double* out, int64_t n, void* 
   ALTO_LAUNCH_CHECK("alto_cast_f32_f64");
   return ALTO_OK;
 }
+
+// ---- deterministic fixed-point MTTKRP support ---------------------------------
+namespace alto {
+template <typename T, bool MAX>
+__global__ void __launch_bounds__(kRedThreads) abs_partial(const T* __restrict__ v, long long n,
+                                                           double* __restrict__ part) {
+  __shared__ double s_tmp[32];
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  double s = 0.0;
+  for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const double x = fabs(static_cast<double>(v[i]));
+    s = MAX ? fmax(s, x) : s + x;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double y = __shfl_down_sync(0xffffffffu, s, o);
+    s = MAX ? fmax(s, y) : s + y;
+  }
+  if (lane == 0) s_tmp[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = MAX ? fmax(t, s_tmp[w]) : t + s_tmp[w];
+    part[blockIdx.x] = t;
+  }
+}
+template <bool MAX>
+__global__ void abs_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x) return;
+  double t = 0.0;
+  for (int b = 0; b < nb; ++b) t = MAX ? fmax(t, part[b]) : t + part[b];
+  *out = t;
+}
+__global__ void fixed_scale_kernel(const double* __restrict__ terms, int nt, double* __restrict__ scale) {
+  if (threadIdx.x) return;
+  double b = 1.0;
+  for (int i = 0; i < nt; ++i) b *= terms[i];
+  if (!(b > 0.0) || !isfinite(b)) b = 1.0;
+  int e = 0;
+  frexp(b, &e);                  // b < 2^e
+  *scale = ldexp(1.0, 61 - e);   // every partial sum < 2^61 in fixed point
+}
+__global__ void fixed_to_float_kernel(const long long* __restrict__ in, const double* __restrict__ scale,
+                                      void* __restrict__ out, int o32, long long n) {
+  const double inv = 1.0 / *scale;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const double x = static_cast<double>(in[i]) * inv;
+    if (o32) static_cast<float*>(out)[i] = static_cast<float>(x);
+    else static_cast<double*>(out)[i] = x;
+  }
+}
+}  // namespace alto
+
+extern "C" {
+int alto_sumabs(const void* x, int32_t dtype, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(ws && ws_bytes >= kRedBlocks * sizeof(double), "workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  if (dtype == ALTO_F32)
+    abs_partial<float, false><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const float*>(x), n, part);
+  else
+    abs_partial<double, false><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const double*>(x), n, part);
+  abs_final<false><<<1, 32, 0, s>>>(part, kRedBlocks, out);
+  ALTO_LAUNCH_CHECK("alto_sumabs");
+  return ALTO_OK;
+}
+int alto_absmax(const void* x, int32_t dtype, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(ws && ws_bytes >= kRedBlocks * sizeof(double), "workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* part = static_cast<double*>(ws);
+  if (dtype == ALTO_F32)
+    abs_partial<float, true><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const float*>(x), n, part);
+  else
+    abs_partial<double, true><<<kRedBlocks, kRedThreads, 0, s>>>(static_cast<const double*>(x), n, part);
+  abs_final<true><<<1, 32, 0, s>>>(part, kRedBlocks, out);
+  ALTO_LAUNCH_CHECK("alto_absmax");
+  return ALTO_OK;
+}
+int alto_fixed_scale(const double* terms, int32_t nterms, double* scale, void* stream) {
+  fixed_scale_kernel<<<1, 32, 0, as_stream(stream)>>>(terms, nterms, scale);
+  ALTO_LAUNCH_CHECK("alto_fixed_scale");
+  return ALTO_OK;
+}
+int alto_fixed_to_float(const int64_t* in, const double* scale, void* out, int32_t out_dtype, int64_t n,
+                        void* stream) {
+  if (n <= 0) return ALTO_OK;
+  fixed_to_float_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const long long*>(in), scale, out, out_dtype == ALTO_F32, n);
+  ALTO_LAUNCH_CHECK("alto_fixed_to_float");
+  return ALTO_OK;
+}
+}  // extern "C"

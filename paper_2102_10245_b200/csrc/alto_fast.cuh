@@ -10,9 +10,40 @@
 // 32-bit funnel shifts and ORs table entries three at a time, and the merge
 // address is formed only when a run ends.
 #pragma once
+#include <type_traits>
+
 #include "alto_stream.cuh"
 
 namespace alto {
+
+
+// Row merge of one lane group's 4-rank partial (G lanes, ranks 4*gl..4*gl+3):
+//  float  -> one RED.F32x4 per lane;
+//  double -> 4x4 in-quad transpose, then fp64 REDs covering one sector each;
+//  long long (deterministic mode) -> round to fixed point (x * scale, scale a
+//            power of two chosen so no partial sum can overflow), transpose,
+//            integer REDs: integer addition is associative, so the merged
+//            result does not depend on the order in which tiles arrive.
+template <typename O, typename A, int G, int R>
+__device__ __forceinline__ void merge_row(O* base, const A (&acc)[4], int gl, unsigned qmask, int lane,
+                                          double scale) {
+  if constexpr (std::is_same<O, float>::value) {
+    red_f32x4(reinterpret_cast<float*>(base), acc, 4 * gl, R, true);
+  } else if constexpr (std::is_same<O, double>::value) {
+    red_f64_sectors(reinterpret_cast<double*>(base), acc, 4 * gl, R, G, qmask, lane);
+  } else {
+    static_assert(G >= 4 && R % 16 == 0, "fixed-point merge needs full lane quads");
+    long long v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __double2ll_rn(static_cast<double>(acc[q]) * scale);
+    const int l = lane & 3;
+    quad_transpose(v, qmask, l);
+    const int b0 = 4 * gl - 4 * l;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      atomicAdd(reinterpret_cast<unsigned long long*>(base + b0 + 4 * q + l), static_cast<unsigned long long>(v[q]));
+  }
+}
 
 constexpr int kFastTile = 128;  // elements per warp sub-tile
 constexpr int kFastBins = 512;
@@ -95,6 +126,7 @@ fast_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ ta
   const int db = L.dec_bytes;
   const V* __restrict__ vals = static_cast<const V*>(P.values);
   O* __restrict__ out = static_cast<O*>(P.out);
+  const double fixed_scale = P.fixed_scale ? *P.fixed_scale : 1.0;
   const int* __restrict__ hot_slot = P.n_hot > 0 ? P.hot_slot : nullptr;
   constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));  // factor row bytes
   // swizzled record address (words): chunk c shifted by 16*c bytes
@@ -243,11 +275,7 @@ fast_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ ta
     int cur = INT_MIN;
     auto flush = [&]() {
       O* base = cur >= 0 ? out + static_cast<long long>(cur) * R : hot_base + static_cast<long long>(-cur - 1) * R;
-      if constexpr (sizeof(O) == 4) {
-        red_f32x4(reinterpret_cast<float*>(base), acc, 4 * gl, R, true);
-      } else {
-        red_f64_sectors(reinterpret_cast<double*>(base), acc, 4 * gl, R, G, qmask, lane);
-      }
+      merge_row<O, A, G, R>(base, acc, gl, qmask, lane, fixed_scale);
     };
     auto consume = [&](const unsigned (&cw)[NW], const V4<F> (&g)[NIN]) {
       const int tg = static_cast<int>(cw[RL::TGT]);
@@ -439,6 +467,7 @@ planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__
   for (int n = 0; n < N; ++n) { pack_off[n] = L.pack_off[n]; bits[n] = L.bits[n]; }
   const V* __restrict__ vals = static_cast<const V*>(P.values);
   O* __restrict__ out = static_cast<O*>(P.out);
+  const double fixed_scale = P.fixed_scale ? *P.fixed_scale : 1.0;
   const int* __restrict__ hot_slot = P.n_hot > 0 ? P.hot_slot : nullptr;
   constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
   auto rec_addr = [](int j) { return j * NW + (j / CH) * 4; };
@@ -518,11 +547,7 @@ planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__
     int cur = INT_MIN;
     auto flush = [&]() {
       O* base = cur >= 0 ? out + static_cast<long long>(cur) * R : hot_base + static_cast<long long>(-cur - 1) * R;
-      if constexpr (sizeof(O) == 4) {
-        red_f32x4(reinterpret_cast<float*>(base), acc, 4 * gl, R, true);
-      } else {
-        red_f64_sectors(reinterpret_cast<double*>(base), acc, 4 * gl, R, G, qmask, lane);
-      }
+      merge_row<O, A, G, R>(base, acc, gl, qmask, lane, fixed_scale);
     };
     auto consume = [&](const unsigned (&cw)[NW], const V4<F> (&g)[NIN]) {
       const int tg = static_cast<int>(cw[RL::TGT]);
@@ -714,6 +739,7 @@ planned2_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict_
   for (int n = 0; n < N; ++n) { pack_off[n] = L.pack_off[n]; bits[n] = L.bits[n]; }
   const V* __restrict__ vals = static_cast<const V*>(P.values);
   O* __restrict__ out = static_cast<O*>(P.out);
+  const double fixed_scale = P.fixed_scale ? *P.fixed_scale : 1.0;
   auto rec_addr = [](int j) { return j * NW + (j / CH) * 4; };
 
   const long long nsub = (P.m + kPlanTile - 1) / kPlanTile;
@@ -772,11 +798,7 @@ planned2_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict_
     int cur = INT_MIN;
     auto flush = [&]() {
       O* base = cur >= 0 ? out + static_cast<long long>(cur) * R : hot_base + static_cast<long long>(-cur - 1) * R;
-      if constexpr (sizeof(O) == 4) {
-        red_f32x4(reinterpret_cast<float*>(base), acc, 4 * gl, R, true);
-      } else {
-        red_f64_sectors(reinterpret_cast<double*>(base), acc, 4 * gl, R, G, qmask, lane);
-      }
+      merge_row<O, A, G, R>(base, acc, gl, qmask, lane, fixed_scale);
     };
     // hot input row -> shared-memory cache, cold row -> read-only global path;
     // both loads sit in one predicated asm block (no branch), so the U x NIN

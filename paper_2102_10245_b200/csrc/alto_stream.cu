@@ -1,5 +1,7 @@
 // alto_stream.cu — C ABI of the streaming ALTO MTTKRP (see alto_stream.cuh
 // for the kernel design), the hot-row plan and the hot-copy reduction.
+#include <type_traits>
+
 #include "alto_fast.cuh"
 
 namespace alto {
@@ -11,11 +13,12 @@ namespace alto {
 template <typename O>
 __global__ void __launch_bounds__(256) hot_reduce_kernel(O* __restrict__ buf, const int* __restrict__ hot_rows,
                                                          int n_hot, int copies, int R, O* __restrict__ out) {
-  __shared__ double s_part[8][33];
+  using S = typename std::conditional<std::is_same<O, long long>::value, long long, double>::type;
+  __shared__ S s_part[8][33];
   const long long n = static_cast<long long>(n_hot) * R;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const long long i = static_cast<long long>(blockIdx.x) * 32 + lane;
-  double s = 0.0;
+  S s = S(0);
   if (i < n) {
     // loads first, then the zeroing stores (no load-after-store chains)
     constexpr int B = 8;
@@ -29,7 +32,7 @@ __global__ void __launch_bounds__(256) hot_reduce_kernel(O* __restrict__ buf, co
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const int k = k0 + 8 * u;
-        s += static_cast<double>(v[u]);
+        s += static_cast<S>(v[u]);
         if (k < copies) buf[k * n + i] = O(0);
       }
     }
@@ -37,12 +40,12 @@ __global__ void __launch_bounds__(256) hot_reduce_kernel(O* __restrict__ buf, co
   s_part[g][lane] = s;
   __syncthreads();
   if (g == 0 && i < n) {
-    double t = 0.0;
+    S t = S(0);
 #pragma unroll
     for (int q = 0; q < 8; ++q) t += s_part[q][lane];
     const long long h = i / R;
     O* o = out + static_cast<long long>(hot_rows[h]) * R + (i - h * R);
-    *o = static_cast<O>(static_cast<double>(*o) + t);
+    *o = static_cast<O>(static_cast<S>(*o) + t);
   }
 }
 
@@ -80,9 +83,10 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   ALTO_REQUIRE(a->rank >= 1, "rank must be positive");
   ALTO_REQUIRE((a->value_dtype == ALTO_F32 || a->value_dtype == ALTO_F64) &&
                    (a->factor_dtype == ALTO_F32 || a->factor_dtype == ALTO_F64) &&
-                   (a->out_dtype == ALTO_F32 || a->out_dtype == ALTO_F64),
+                   (a->out_dtype == ALTO_F32 || a->out_dtype == ALTO_F64 || a->out_dtype == ALTO_I64),
                "unsupported dtype");
-  ALTO_REQUIRE(a->out_dtype == ALTO_F64 || (a->value_dtype == ALTO_F32 && a->factor_dtype == ALTO_F32),
+  ALTO_REQUIRE(a->out_dtype != ALTO_I64 || a->fixed_scale != nullptr, "fixed-point output needs fixed_scale");
+  ALTO_REQUIRE(a->out_dtype != ALTO_F32 || (a->value_dtype == ALTO_F32 && a->factor_dtype == ALTO_F32),
                "float32 output needs float32 values and factors");
   ALTO_REQUIRE(a->out != nullptr, "out is NULL");
   ALTO_REQUIRE(a->n_hot <= 0 || (a->hot_rows && a->hot_slot && a->hot_buf && a->hot_copies > 0),
@@ -92,7 +96,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   const DevLayout d = make_dev_layout(a->lay);
   cudaStream_t s = as_stream(stream);
   const long long dim = d.dims[a->mode];
-  const size_t osz = a->out_dtype == ALTO_F32 ? 4 : 8;
+  const size_t osz = a->out_dtype == ALTO_F32 ? 4 : 8;  // f64 and i64 are 8 bytes
   if (a->zero_out) ALTO_CUDA_TRY(cudaMemsetAsync(a->out, 0, static_cast<size_t>(dim) * a->rank * osz, s));
   if (a->m <= 0) return ALTO_OK;
   StreamParams P{};
@@ -115,6 +119,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.flags = a->flags;
   P.packed = a->packed;
   P.pos = a->pos;
+  P.fixed_scale = a->out_dtype == ALTO_I64 ? a->fixed_scale : nullptr;
   Plan2 pl2{};
   P.plan2 = nullptr;
   if (a->plan) {
@@ -128,6 +133,23 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   }
   const auto* tab = static_cast<const uint64_t*>(a->d_tables);
   const bool o32 = a->out_dtype == ALTO_F32;
+  if (a->out_dtype == ALTO_I64) {
+    int sti = d.n_words == 1 ? fast_w1_i64(d, tab, P, a->value_dtype, a->factor_dtype, s)
+                             : fast_w2_i64(d, tab, P, a->value_dtype, a->factor_dtype, s);
+    if (sti == ALTO_EUNSUPPORTED) {
+      set_error("fixed-point (deterministic) MTTKRP supports orders 3-5 and ranks 16/32 with matching dtypes");
+      return ALTO_EUNSUPPORTED;
+    }
+    if (sti) return sti;
+    if (P.n_hot > 0) {
+      const long long nh = static_cast<long long>(P.n_hot) * a->rank;
+      hot_reduce_kernel<long long><<<static_cast<int>((nh + 31) / 32), 256, 0, s>>>(
+          static_cast<long long*>(P.hot_buf), a->hot_rows, P.n_hot, P.hot_copies, a->rank,
+          static_cast<long long*>(a->out));
+      ALTO_LAUNCH_CHECK("alto_mttkrp/hot_reduce");
+    }
+    return ALTO_OK;
+  }
   int st = d.n_words == 1 ? (o32 ? fast_w1_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
                                  : fast_w1_f64(d, tab, P, a->value_dtype, a->factor_dtype, s))
                           : (o32 ? fast_w2_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)

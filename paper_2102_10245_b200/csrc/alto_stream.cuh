@@ -61,7 +61,8 @@ struct StreamParams {
   int flags;
   const uint64_t* packed;     // mode-contiguous keys (optional, alto_pack_keys)
   const unsigned char* pos;   // per-mode sub-tile slots (optional, alto_subtile_order)
-  const Plan2* plan2;         // per-mode plan words + hot-input caches (optional, host struct)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
+  const Plan2* plan2;         // per-mode plan words + hot-input caches (optional, host struct)
+  const double* fixed_scale;  // deterministic mode: device scalar, int64 output = round(x * scale)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
 };
 
 template <typename V, typename F>
@@ -866,6 +867,8 @@ int fast_w1_f32(const DevLayout&, const uint64_t*, const StreamParams&, int vd, 
 int fast_w1_f64(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
 int fast_w2_f32(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
 int fast_w2_f64(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
+int fast_w1_i64(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
+int fast_w2_i64(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
 int stream_w1_f32(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
 int stream_w1_f64(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);
 int stream_w2_f32(const DevLayout&, const uint64_t*, const StreamParams&, int vd, int fd, cudaStream_t);

@@ -89,18 +89,19 @@ def _dt_code(t) -> int:
     return _lib.ALTO_F32 if t.dtype == torch.float32 else _lib.ALTO_F64
 
 
-def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_out: int = 1):
+def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_out: int = 1, vals=None):
     lay = tensor.layout
+    vals = tensor.vals if vals is None else vals
     a = _lib.CMttkrpArgs()
     cl = c_layout(lay)
     a.lay = ctypes.pointer(cl)
     a.d_tables = device_tables(lay).data_ptr()
     a.keys = tensor.keys.data_ptr()
-    a.values = tensor.vals.data_ptr()
+    a.values = vals.data_ptr()
     a.m = tensor.nnz
     a.mode = mode
     a.rank = int(fdev[0].shape[1])
-    a.value_dtype = _dt_code(tensor.vals)
+    a.value_dtype = _dt_code(vals)
     fdt = {_dt_code(f) for f in fdev}
     if len(fdt) != 1:
         raise ValueError("factor matrices must share one dtype")
@@ -113,6 +114,7 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
     a.zero_out = zero_out
     a.n_hot = 0
     a.flags = STREAM_FLAGS
+    a.fixed_scale = None
     a.packed = None
     a.pos = None
     a.plan = None
@@ -325,6 +327,99 @@ def row_index(tensor: AltoTensor, mode: int):
     return perm, ptr
 
 
+# Rows longer than this make the exact-order engine's sequential per-row sums
+# slow (a Zipf head row of 6.5M elements takes ~3 s); above it the
+# deterministic fixed-point streaming path is used instead.
+EXACT_MAX_RUN = int(__import__("os").environ.get("ALTO_EXACT_MAX_RUN", 65536))
+
+
+def max_row_length(tensor: AltoTensor, mode: int) -> int:
+    key = ("maxrun", mode)
+    hit = tensor._cache.get(key)
+    if hit is None:
+        _perm, ptr = row_index(tensor, mode)
+        hit = int((ptr[1:] - ptr[:-1]).max().item()) if ptr.numel() > 1 else 0
+        tensor._cache[key] = hit
+    return hit
+
+
+def det_supported(tensor: AltoTensor, fdev: list) -> bool:
+    torch = _torch()
+    lay = tensor.layout
+    rank = int(fdev[0].shape[1])
+    return tensor.nnz > 0 and rank in (16, 32) and 3 <= lay.order <= 5 and max(lay.bits) <= 31
+
+
+def mttkrp_det(tensor: AltoTensor, fdev: list, mode: int, out=None):
+    """Deterministic streaming MTTKRP -> (I_mode, R) float64 device tensor.
+
+    Same kernel as mttkrp_stream, but row partials are merged as int64 fixed
+    point (scale = a power of two from the bound sum|v| * prod max|F|):
+    integer addition is associative, so the result is bitwise identical for
+    every run, tile order, worker or partition count."""
+    torch = _torch()
+    lib = _lib.load()
+    dev = tensor.keys.device
+    rank = int(fdev[0].shape[1])
+    dim = tensor.layout.dims[mode]
+    vals = tensor.vals
+    if fdev[0].dtype != vals.dtype:
+        # mixed precision: compute in float64 (upcasting float32 is exact)
+        if vals.dtype == torch.float32:
+            vals = tensor._cache.get("vals64")
+            if vals is None:
+                vals = tensor.vals.double()
+                tensor._cache["vals64"] = vals
+        else:
+            fdev = [f.double() for f in fdev]
+    ws = tensor._cache.get("det_ws")
+    if ws is None:
+        nb = int(lib.alto_cpd_workspace_bytes(1))
+        ws = (torch.empty(nb, dtype=torch.uint8, device=dev), nb,
+              torch.empty(_lib.ALTO_MAX_ORDER + 1, dtype=torch.float64, device=dev),
+              torch.empty(1, dtype=torch.float64, device=dev))
+        code = _lib.ALTO_F32 if tensor.vals.dtype == torch.float32 else _lib.ALTO_F64
+        _lib.check(lib.alto_sumabs(tensor.vals.data_ptr(), code, tensor.nnz, ws[2].data_ptr(), ws[0].data_ptr(), nb,
+                                   _lib.stream_ptr()), "alto_sumabs")
+        tensor._cache["det_ws"] = ws
+    buf, nb, terms, scale = ws
+    k = 1
+    for n, f in enumerate(fdev):
+        if n == mode:
+            continue
+        code = _lib.ALTO_F32 if f.dtype == torch.float32 else _lib.ALTO_F64
+        _lib.check(lib.alto_absmax(f.data_ptr(), code, f.numel(), terms[k:].data_ptr(), buf.data_ptr(), nb,
+                                   _lib.stream_ptr()), "alto_absmax")
+        k += 1
+    _lib.check(lib.alto_fixed_scale(terms.data_ptr(), k, scale.data_ptr(), _lib.stream_ptr()), "alto_fixed_scale")
+    fixed = torch.empty((dim, rank), dtype=torch.int64, device=dev)
+    a, _keep = _args(tensor, fdev, mode, fixed, DEFAULT_TILE, 1, vals=vals)
+    a.out_dtype = _lib.ALTO_I64
+    a.fixed_scale = scale.data_ptr()
+    a.packed = packed_keys(tensor).data_ptr()
+    a.pos = subtile_order(tensor, mode).data_ptr()
+    hp = hot_plan(tensor, mode, rank, torch.int64)
+    if hp is not None:
+        slot, rows, n, copies, hbuf = hp
+        a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf = (slot.data_ptr(), rows.data_ptr(), n, copies,
+                                                                   hbuf.data_ptr())
+    _lib.check(lib.alto_mttkrp(ctypes.byref(a), _lib.stream_ptr()), "alto_mttkrp(deterministic)")
+    if out is None:
+        out = torch.empty((dim, rank), dtype=torch.float64, device=dev)
+    _lib.check(lib.alto_fixed_to_float(fixed.data_ptr(), scale.data_ptr(), out.data_ptr(), _dt_code(out),
+                                       fixed.numel(), _lib.stream_ptr()), "alto_fixed_to_float")
+    return out
+
+
+def mttkrp_deterministic(tensor: AltoTensor, fdev: list, mode: int, part_offsets=None, out=None):
+    """Deterministic MTTKRP: the exact-order engine (bitwise equal to the
+    reference) when the longest row is short, else the fixed-point streaming
+    kernel (bitwise reproducible, ~1e-13 relative to the exact sums)."""
+    if tensor.nnz > 0 and det_supported(tensor, fdev) and max_row_length(tensor, mode) > EXACT_MAX_RUN:
+        return mttkrp_det(tensor, fdev, mode, out=out)
+    return mttkrp_exact(tensor, fdev, mode, part_offsets, out=out)
+
+
 def mttkrp_exact(tensor: AltoTensor, fdev: list, mode: int, part_offsets=None, out=None):
     """Deterministic exact-order MTTKRP -> (I_mode, R) float64 device tensor."""
     torch = _torch()
@@ -372,7 +467,7 @@ def mttkrp_seq(tensor: AltoTensor, factors, mode: int):
     """Sequential-order MTTKRP (mttkrp.py:108-117): exact-order engine, one partition."""
     _check_factors(tensor.layout.dims, factors, mode)
     fdev = factors_to_device(factors)
-    return _finish(mttkrp_exact(tensor, fdev, mode), any(_is_torch(f) for f in factors))
+    return _finish(mttkrp_deterministic(tensor, fdev, mode), any(_is_torch(f) for f in factors))
 
 
 def _any_flag(tensor: AltoTensor, flag_bit: int) -> bool:
@@ -399,7 +494,7 @@ def mttkrp_par(tensor: AltoTensor, parts: PartitionSet, plan: ConflictPlan, fact
     fdev = factors_to_device(factors)
     like = any(_is_torch(f) for f in factors)
     if plan.strategy is Strategy.BUFFERED:
-        return _finish(mttkrp_exact(tensor, fdev, mode, np.asarray(parts.offsets)), like)
+        return _finish(mttkrp_deterministic(tensor, fdev, mode, np.asarray(parts.offsets)), like)
     if plan.flag_bit is not None and plan.overlaps is not None and any(plan.overlaps) and tensor.nnz:
         if not _any_flag(tensor, plan.flag_bit):
             raise ValueError("plan expects boundary flags; apply_boundary_flags first")

@@ -262,6 +262,32 @@ class TestStreamKernel:
                 a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=variant).double().cpu().numpy()
                 assert rel_error(a, b) <= 1e-6, variant
 
+    @pytest.mark.parametrize("cfg,rank", [(2, 16), (3, 32), ("wide", 16), (1, 16)])
+    def test_deterministic_fixed_point(self, at, monkeypatch, cfg, rank):
+        """Fixed-point streaming mode (used for Buffered / seq when rows are
+        long): bitwise identical across runs, ~1e-13 from the fp64 oracle."""
+        import importlib
+
+        mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+
+        monkeypatch.setattr(mk, "EXACT_MAX_RUN", 0)  # force the fixed-point path at test size
+        st = synth.make_tensor(self.WIDE if cfg == "wide" else cfg, nnz=150_000)
+        dims = st.config.dims
+        fp32 = st.config.value_dtype == "float32"
+        alto = at.build_alto(at.CooTensor(dims, st.coords, st.values.astype(np.float64)),
+                             dtype="float32" if fp32 else "float64")
+        factors = seeded_factors(dims, rank, 21)
+        for mode in range(len(dims)):
+            a = at.mttkrp_seq(alto, factors, mode)
+            b = at.mttkrp_seq(alto, factors, mode)
+            assert np.array_equal(a, b)
+            ref = orc.mttkrp_coo(st.coords, st.values.astype(np.float64), factors, mode)
+            assert rel_error(a, ref) <= 1e-12, rel_error(a, ref)
+            parts = at.partition(alto, 6)
+            plan = at.plan_conflicts(alto, parts, mode, force_strategy=at.Strategy.BUFFERED)
+            c = at.mttkrp_par(alto, parts, plan, factors, mode, workers=3)
+            assert np.array_equal(a, c)
+
     def test_accumulates_into_out(self, at):
         from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
 
