@@ -200,6 +200,12 @@ int alto_fixed_to_float(const int64_t* in, const double* scale, void* out, int32
 size_t alto_topk_rows_workspace_bytes(int64_t dim);
 int alto_topk_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int32_t* rows, int32_t* slot_map, void* ws,
                    size_t ws_bytes, void* stream);
+/* Hot-row plan by rank: the (up to) k rows with the most elements, keeping
+ * only rows with more than min_count; slots 0..*d_count-1 in descending
+ * count order (rows -1 padded; slot_map dim int32: slot or -1).  Same
+ * workspace as alto_topk_rows. */
+int alto_hot_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int64_t min_count, int32_t* rows,
+                  int32_t* slot_map, int32_t* d_count, void* ws, size_t ws_bytes, void* stream);
 /* Per-mode plan words (see alto_fast.cuh, planned variant 2): slot in the
  * 256-element sub-tile after a stable counting sort by `mode` coordinate,
  * hot-input slots for up to 3 input modes (in_slot_maps_host: host array of

@@ -91,6 +91,8 @@ SIGNATURES = [
     ("alto_subtile_order", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_topk_rows_workspace_bytes", c_size_t, [c_int64]),
     ("alto_topk_rows", c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("alto_hot_rows", c_int32, [c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_size_t, c_void_p]),
     ("alto_stream_plan", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, POINTER(c_void_p), c_void_p,
                                    c_void_p, c_void_p]),
     ("alto_hot_plan", c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -260,14 +260,21 @@ __global__ void topk_keys_kernel(const long long* __restrict__ row_ptr, long lon
   }
 }
 
-__global__ void topk_finish_kernel(const uint64_t* __restrict__ sorted, long long dim, int k, int* __restrict__ rows,
-                                   int* __restrict__ slot_map) {
-  for (int s = threadIdx.x; s < k; s += blockDim.x) {
+__global__ void topk_finish_kernel(const uint64_t* __restrict__ sorted, long long dim, int k,
+                                   unsigned long long min_count, int* __restrict__ rows, int* __restrict__ slot_map,
+                                   int* __restrict__ count) {
+  // sorted ascending: slot s holds the s-th largest count; rows with count
+  // <= min_count get no slot, so assigned slots form the prefix [0, *count)
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < k; s += gridDim.x * blockDim.x) {
     const long long idx = dim - 1 - s;
     int r = -1;
-    if (idx >= 0 && (sorted[idx] >> 32) > 0) r = static_cast<int>(0xffffffffull - (sorted[idx] & 0xffffffffull));
+    if (idx >= 0 && (sorted[idx] >> 32) > min_count)
+      r = static_cast<int>(0xffffffffull - (sorted[idx] & 0xffffffffull));
     rows[s] = r;
-    if (r >= 0) slot_map[r] = s;
+    if (r >= 0) {
+      slot_map[r] = s;
+      if (count) atomicMax(count, s + 1);
+    }
   }
 }
 
@@ -298,8 +305,28 @@ int alto_topk_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int32_t* rows
   ALTO_LAUNCH_CHECK("alto_topk_rows");
   const int st = alto_sort_pairs(keys, nullptr, dim, 1, 0, 64, static_cast<char*>(ws) + a, ws_bytes - a, stream);
   if (st) return st;
-  topk_finish_kernel<<<1, 256, 0, s>>>(keys, dim, k, rows, slot_map);
+  topk_finish_kernel<<<1, 256, 0, s>>>(keys, dim, k, 0ull, rows, slot_map, nullptr);
   ALTO_LAUNCH_CHECK("alto_topk_rows/finish");
+  return ALTO_OK;
+}
+
+int alto_hot_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int64_t min_count, int32_t* rows,
+                  int32_t* slot_map, int32_t* d_count, void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(dim >= 1 && dim <= INT_MAX, "hot rows need 1 <= dim < 2^31");
+  ALTO_REQUIRE(k >= 1 && k <= (1 << 20), "hot rows k must be in [1, 2^20]");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_topk_rows_workspace_bytes(dim), "hot rows workspace too small");
+  cudaStream_t s = as_stream(stream);
+  auto* keys = static_cast<uint64_t*>(ws);
+  const size_t a = (static_cast<size_t>(dim) * 8 + 255) & ~size_t(255);
+  topk_keys_kernel<<<grid_for(dim, 256), 256, 0, s>>>(reinterpret_cast<const long long*>(row_ptr), dim, keys);
+  fill_i32<<<grid_for(dim, 256), 256, 0, s>>>(slot_map, dim, -1);
+  ALTO_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(int32_t), s));
+  ALTO_LAUNCH_CHECK("alto_hot_rows");
+  const int st = alto_sort_pairs(keys, nullptr, dim, 1, 0, 64, static_cast<char*>(ws) + a, ws_bytes - a, stream);
+  if (st) return st;
+  topk_finish_kernel<<<grid_for(k, 256), 256, 0, s>>>(keys, dim, k, static_cast<unsigned long long>(min_count), rows,
+                                                       slot_map, d_count);
+  ALTO_LAUNCH_CHECK("alto_hot_rows/finish");
   return ALTO_OK;
 }
 

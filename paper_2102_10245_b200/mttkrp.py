@@ -127,7 +127,7 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
 # tile; their tile partials go to HOT_COPIES replicated buffers instead of
 # contending on one L2 line (see alto_mttkrp_args in include/alto_b200.h).
 HOT_TAU = 1024
-HOT_MAX = 8192
+HOT_MAX = 32768
 # float32 copies take fewer adds each (precision); float64 copies fewer bytes
 HOT_COPIES = {4: 64, 8: 32}
 
@@ -146,10 +146,14 @@ def hot_slots(tensor: AltoTensor, mode: int):
         dev = tensor.keys.device
         _perm, ptr = row_index(tensor, mode)
         slot = torch.empty(dim, dtype=torch.int32, device=dev)
-        rows = torch.empty(HOT_MAX, dtype=torch.int32, device=dev)
+        kk = min(HOT_MAX, dim)
+        rows = torch.empty(kk, dtype=torch.int32, device=dev)
         nhot = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.check(lib.alto_hot_plan(ptr.data_ptr(), dim, HOT_TAU, HOT_MAX, slot.data_ptr(), rows.data_ptr(),
-                                     nhot.data_ptr(), _lib.stream_ptr()), "alto_hot_plan")
+        wsb = lib.alto_topk_rows_workspace_bytes(dim)
+        ws = torch.empty(int(wsb), dtype=torch.uint8, device=dev)
+        # the HOT_MAX rows with the most elements, if above HOT_TAU (hottest first)
+        _lib.check(lib.alto_hot_rows(ptr.data_ptr(), dim, kk, HOT_TAU, rows.data_ptr(), slot.data_ptr(),
+                                     nhot.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()), "alto_hot_rows")
         n = int(nhot.item())
         if n > 0:
             res = (slot, rows, n)

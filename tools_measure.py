@@ -65,9 +65,32 @@ def cpals5(nnz, iters):
     print(f"peak memory {torch.cuda.max_memory_allocated() / 2**30:.1f} GiB")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and sys.argv[1] != "cpals":
     what = sys.argv[1]
     if what == "exact":
         exact(int(sys.argv[2]) if len(sys.argv) > 2 else 50_000_000, len(sys.argv) <= 3)
     else:
         cpals5(int(sys.argv[2]) if len(sys.argv) > 2 else 500_000_000, int(sys.argv[3]) if len(sys.argv) > 3 else 10)
+
+
+def cpals_breakdown(cfg_id=2, nnz=None, iters=3):
+    """CP-ALS sweeps on device (streaming backend) for an ncu launch list."""
+    from paper_2102_10245_b200.cpd import DeviceCpAls
+
+    cfg = synth.CONFIGS[cfg_id]
+    coords, vals = synth.make_tensor_device(cfg_id, nnz=nnz)
+    alto = build_alto_device(build_masks(cfg.dims), coords, vals)
+    st = DeviceCpAls(alto, cfg.rank, seed=0, backend="atomic", partitions=8)
+    st.sweep()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        st.sweep()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{cfg.name}: CP-ALS {e0.elapsed_time(e1) / iters:.2f} ms/iter", flush=True)
+
+
+if __name__ == "__main__" and sys.argv[1] == "cpals":
+    cpals_breakdown(int(sys.argv[2]))
