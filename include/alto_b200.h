@@ -181,6 +181,18 @@ typedef struct alto_mttkrp_args {
   int32_t cache_k;
   int32_t cache_modes;
   const double* fixed_scale;     /* device scalar for ALTO_I64 output (alto_fixed_scale) */
+  /* Per-mode stream (built by alto_mode_stream for this mode): keys, values
+   * and its tile length.  When set, the mode-stream kernel runs (orders 3-5,
+   * ranks 16/32, max_n I_n*rank*sizeof(factor) < 2^32; else ALTO_EUNSUPPORTED)
+   * and, for ALTO_F32 output, hot_buf holds float64 copies. */
+  const uint64_t* mkeys;
+  const void* mvals;
+  int32_t mtile;
+  /* Mode-stream hot plan (alto_hot_copies): with mkeys set, hot_slot holds
+   * hot_code (dim int32: (first copy << 5) | log2(copies), or -1), hot_base
+   * the per-slot first copy (n_hot+1), and hot_buf hot_base[n_hot] * rank
+   * elements of out_dtype (zero on entry, left zero). */
+  const int32_t* hot_base;
 } alto_mttkrp_args;
 
 /* Deterministic MTTKRP support (ALTO_I64 output).  alto_sumabs / alto_absmax:
@@ -224,6 +236,33 @@ int alto_pack_keys(const alto_layout* lay, const void* d_tables, const uint64_t*
 int alto_subtile_order(const alto_layout* lay, const uint64_t* packed, int64_t m, int32_t mode, uint8_t* pos,
                        void* stream);
 
+/* Per-mode stream of the MTTKRP (alto_mstream.cuh), built once per tensor
+ * and mode like the reference's per-mode plans / flagged key copies
+ * (_make_backend, cpd.py:149-181): the sorted ALTO stream cut into tiles of
+ * `tile` consecutive elements (contiguous key ranges), each tile stably
+ * sorted by its `mode` coordinate and split into 8 slices of tile/8 elements
+ * stored interleaved (sorted position p of tile t at t*tile + (p % (tile/8))*8
+ * + p / (tile/8)).  Keys hold the element's coordinates re-packed for the
+ * mode — input modes ascending, then `mode`, from bit 0, no field straddling
+ * a 64-bit word — and, when hot_slot (dim int32, slot or -1) is given, bit
+ * 64*n_words-1 set on elements of hot rows.  Returns ALTO_EUNSUPPORTED when
+ * that layout does not fit below bit 64*n_words-1.  skeys / svals
+ * hold ceil(m/tile)*tile elements (the tail is zero padding).  value_dtype
+ * ALTO_F32 or ALTO_F64; tile a multiple of 256 with m / tile < 2^31. */
+size_t alto_mode_stream_workspace_bytes(int64_t m);
+int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,
+                     int64_t m, int32_t mode, int32_t tile, const int32_t* hot_slot, uint64_t* skeys,
+                     void* svals, void* ws, size_t ws_bytes, void* stream);
+
+/* Hot-row copy plan of the mode-stream kernel: hot row s (hot_rows[s],
+ * from alto_hot_rows) gets copies = 2^lg replicated partial rows, lg the
+ * smallest with 2^lg * bound >= estimated merges (min(count, tiles) +
+ * count/(tile/8)), lg <= max_lg; copies are laid out slot by slot:
+ * hot_base[s] = first copy (n_hot+1 entries), hot_code[row] = (hot_base << 5)
+ * | lg.  hot_code must be pre-filled with -1 for the other rows. */
+int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_hot, int64_t m, int32_t tile,
+                    int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base, void* stream);
+
 /* Streaming-kernel tuning switches (alto_mttkrp_args.flags). */
 #define ALTO_STREAM_WARP_AGG 1   /* warp-aggregate in-tile sort atomics */
 #define ALTO_STREAM_FULL_BINS 2  /* scan all sort bins instead of the tile span */
@@ -232,6 +271,8 @@ int alto_subtile_order(const alto_layout* lay, const uint64_t* packed, int64_t m
 #define ALTO_STREAM_GENERIC 128  /* bypass the specialised (order 3-5, rank 16/32) kernels */
 #define ALTO_STREAM_TUNE_MINB2 256  /* tuning: 2 CTAs/SM launch bounds (default 3) */
 #define ALTO_STREAM_TUNE_U4 512     /* tuning: 4 elements in flight per group (default 2) */
+#define ALTO_STREAM_MS_COOP 1024    /* tuning: mode-stream kernel with broadcast key loads instead of
+                                       cooperative decode + shuffles (cfg2 shape only) */
 /* Ablation switches for profiling only (results are wrong when set). */
 #define ALTO_STREAM_DBG_NO_RED 8
 #define ALTO_STREAM_DBG_NO_GATHER 16

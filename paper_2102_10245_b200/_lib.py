@@ -62,6 +62,10 @@ class CMttkrpArgs(Structure):
         ("cache_k", c_int32),
         ("cache_modes", c_int32),
         ("fixed_scale", c_void_p),
+        ("mkeys", c_void_p),
+        ("mvals", c_void_p),
+        ("mtile", c_int32),
+        ("hot_base", c_void_p),
     ]
 
 
@@ -89,6 +93,11 @@ SIGNATURES = [
     ("alto_mttkrp", c_int32, [POINTER(CMttkrpArgs), c_void_p]),
     ("alto_pack_keys", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     ("alto_subtile_order", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    ("alto_mode_stream_workspace_bytes", c_size_t, [c_int64]),
+    ("alto_hot_copies", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p,
+                                  c_void_p]),
+    ("alto_mode_stream", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_topk_rows_workspace_bytes", c_size_t, [c_int64]),
     ("alto_topk_rows", c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_hot_rows", c_int32, [c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,

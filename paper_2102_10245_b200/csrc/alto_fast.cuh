@@ -373,6 +373,8 @@ int launch_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, 
 template <int W, typename V, typename O>
 int try_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packed, const unsigned char* pos,
                 cudaStream_t s);
+template <int W, typename V, typename O>
+int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s);
 struct Plan2;
 template <int W, typename V, typename O>
 int try_planned2(const DevLayout& d, const StreamParams& P, const Plan2& PL, cudaStream_t s);
@@ -380,6 +382,12 @@ int try_planned2(const DevLayout& d, const StreamParams& P, const Plan2& PL, cud
 template <int W, typename V, typename O>
 int try_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaStream_t s) {
   if (P.flags & (ALTO_STREAM_CTA_TILES | ALTO_STREAM_GENERIC)) return ALTO_EUNSUPPORTED;
+  if (P.mkeys) {
+    // a mode stream pins the kernel (its hot copies are float64 for float32 output)
+    const int st = try_mstream<W, V, O>(d, P, s);
+    if (st == ALTO_EUNSUPPORTED) set_error("shape not covered by the mode-stream kernel");
+    return st;
+  }
   if (P.packed && P.plan2 && P.plan2->plan) {
     const int st = try_planned2<W, V, O>(d, P, *P.plan2, s);
     if (st != ALTO_EUNSUPPORTED) return st;

@@ -1,5 +1,5 @@
 // Instantiations of the specialised streaming MTTKRP: 1-word keys, f32 output.
-#include "alto_fast.cuh"
+#include "alto_mstream.cuh"
 
 namespace alto {
 

@@ -1,5 +1,5 @@
 // Instantiations of the specialised streaming MTTKRP: 2-word keys, f64 output.
-#include "alto_fast.cuh"
+#include "alto_mstream.cuh"
 
 namespace alto {
 

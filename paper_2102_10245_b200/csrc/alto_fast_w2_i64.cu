@@ -1,6 +1,6 @@
 // Instantiations of the specialised streaming MTTKRP: 2-word keys,
 // deterministic fixed-point (int64) output.
-#include "alto_fast.cuh"
+#include "alto_mstream.cuh"
 
 namespace alto {
 

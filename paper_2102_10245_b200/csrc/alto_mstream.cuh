@@ -1,0 +1,391 @@
+// alto_mstream.cuh — mode-stream MTTKRP: the streaming ALTO MTTKRP over a
+// per-mode copy of the ALTO stream that is already in the order the kernel
+// consumes it.
+//
+// The per-mode stream (built once per tensor and mode by alto_mode_stream,
+// like the reference's per-mode plans and flagged key copies in
+// _make_backend, pkg/src/altotensor/cpd.py:149-181) holds the same elements,
+// keys (mode-contiguous bit order, alto_pack_keys) and values as the sorted
+// ALTO stream, cut into tiles of T consecutive elements — contiguous
+// linearized-key ranges, i.e. ALTO partitions (format.py:127-154) — and, inside
+// each tile, stably sorted by the output-mode coordinate (the per-partition
+// interval buffer of the paper's Buffered scheme, Alg. 2 / mttkrp.py:148-156,
+// at tile granularity) and split into 8 slices of T/8 elements stored
+// interleaved: sorted position p of tile t lives at t*T + (p % CH)*8 + p / CH
+// (CH = T/8).  Rows of the mode's hot plan carry a flag in the key's top bit.
+//
+// Kernel: a warp owns a tile; G = R/4 lanes own one slice each (4 consecutive
+// ranks per lane, a factor row is one contiguous 16*G-byte request); the 8
+// slices of instruction j are 8 consecutive keys/values (one coalesced
+// request each).  Every lane decodes its slice's element with shifts,
+// gathers the N-1 input rows with U elements in flight, forms the Hadamard
+// product and accumulates in registers while the output row repeats; on a
+// row change the partial row is merged with one RED.F32x4 per lane (float32),
+// sector-covering float64 REDs, or int64 fixed-point REDs (deterministic).
+// Hot rows (a Zipf head row is touched by nearly every tile) merge into one of
+// that row's replicated partial rows (tile mod copies; copies per row sized by
+// alto_hot_copies so each receives a bounded number of merges), summed
+// afterwards in a fixed order by hot_reduce_rows_kernel.
+//
+// Compared with planned_kernel (alto_fast.cuh) this removes the in-kernel
+// record pass through shared memory (phase A), the per-element plan byte and
+// hot-slot lookups, and lets tiles be long (1024-4096 elements: fewer row
+// runs, hence fewer merges) because no per-tile state lives on chip.
+#pragma once
+#include "alto_fast.cuh"
+
+namespace alto {
+
+constexpr int kMsSlices = 8;  // slices per tile (lane groups of a rank-16 warp)
+
+template <int W>
+__device__ __forceinline__ Key<W> load_key_stream(const uint64_t* __restrict__ keys, long long i) {
+  Key<W> k;
+  if constexpr (W == 1) {
+    unsigned long long v;
+    asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(keys + i));
+    k.w[0] = v;
+  } else {
+    unsigned long long a, b;
+    asm("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(keys + 2 * i));
+    k.w[0] = a;
+    k.w[1] = b;
+  }
+  return k;
+}
+
+template <typename V>
+__device__ __forceinline__ V load_val_stream(const V* __restrict__ p) {
+  if constexpr (sizeof(V) == 4) {
+    float v;
+    asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+  } else {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+  }
+}
+
+// Field layout of a per-mode stream key: the coordinates of the input modes
+// (ascending) and then of the output mode, packed from bit 0 without any
+// field straddling a 64-bit word; bit 64W-1 is the hot-row flag.
+struct MsFields {
+  int word[ALTO_MAX_ORDER];
+  int sh[ALTO_MAX_ORDER];
+  unsigned mask[ALTO_MAX_ORDER];
+  int ok;  // layout fits below the flag bit
+};
+
+inline MsFields ms_fields(const DevLayout& d, int mode) {
+  MsFields f{};
+  int cur = 0;
+  for (int i = 0; i < d.order; ++i) {
+    const int n = i < d.order - 1 ? (i < mode ? i : i + 1) : mode;
+    const int b = d.bits[n];
+    if ((cur & 63) + b > 64) cur = (cur + 63) & ~63;
+    f.word[n] = cur >> 6;
+    f.sh[n] = cur & 63;
+    f.mask[n] = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
+    cur += b;
+  }
+  f.ok = cur <= 64 * d.n_words - 1;
+  return f;
+}
+
+// One field selector held in registers (hoisted out of the element loops).
+struct FSel {
+  unsigned sh, mask;
+  bool hi;
+};
+
+__device__ __forceinline__ FSel fsel_of(const MsFields& f, int n) { return FSel{static_cast<unsigned>(f.sh[n]), f.mask[n], f.word[n] != 0}; }
+
+template <int W>
+__device__ __forceinline__ unsigned ms_field(const Key<W>& k, const FSel& f) {
+  const uint64_t w = (W == 1 || !f.hi) ? k.w[0] : k.w[W - 1];
+  return static_cast<unsigned>(w >> f.sh) & f.mask;
+}
+
+struct MStream {
+  const uint64_t* keys;  // (ntiles*T, W) stream keys (MsFields layout), hot flag in bit 64W-1
+  const void* vals;      // (ntiles*T,) values
+  int tile;              // T (multiple of 256)
+  MsFields f;
+};
+
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, bool COOP = false>
+__global__ void __launch_bounds__(kTileThreads, MINB)
+mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStream S,
+               const __grid_constant__ StreamParams P) {
+  using F = V;
+  using A = V;
+  constexpr int G = R / 4;          // lanes per element
+  constexpr int GPW = 32 / G;       // slices processed at once by a warp
+  constexpr int PASSES = kMsSlices / GPW;
+  constexpr int NIN = N - 1;
+  constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
+  constexpr unsigned HOTF = 0x80000000u;
+  static_assert(!COOP || (U >= 1 && U <= G), "one decoding lane per element of a block");
+  const int mode = P.mode;
+  const int T = S.tile;
+  const int CH = T / kMsSlices;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const unsigned qmask = (G >= 4) ? (0xFu << (lane & ~3)) : 0xffffffffu;
+  const char* fin_lane[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) {
+    const int n = k < mode ? k : k + 1;
+    fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(P.factors[n]) + 4 * gl);
+  }
+  FSel fin[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) fin[k] = fsel_of(S.f, k < mode ? k : k + 1);
+  const FSel fout = fsel_of(S.f, mode);
+  const V* __restrict__ vals = static_cast<const V*>(S.vals);
+  O* __restrict__ out = static_cast<O*>(P.out);
+  const double fixed_scale = P.fixed_scale ? *P.fixed_scale : 1.0;
+  // hot plan of the mode stream (alto_hot_copies): hot_code[row] = (first copy
+  // << 5) | log2(copies); each hot row has its own power-of-two number of
+  // replicated partial rows, sized so that no copy receives more than a
+  // bounded number of merges (contention and float32 rounding stay bounded)
+  const int* __restrict__ hot_code = P.n_hot > 0 ? P.hot_slot : nullptr;
+  O* __restrict__ hot_buf = static_cast<O*>(P.hot_buf);
+  const unsigned hotmask = hot_code ? HOTF : 0u;  // stream flags are ignored without a hot plan
+
+  const long long ntiles = (P.m + T - 1) / T;
+  const long long gw0 = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp;
+  const long long nwarps = static_cast<long long>(gridDim.x) * (kTileThreads / 32);
+  for (long long t = gw0; t < ntiles; t += nwarps) {
+    const long long tb = t * T;
+    const int cnt = static_cast<int>(min(static_cast<long long>(T), P.m - tb));
+#pragma unroll 1
+    for (int pass = 0; pass < PASSES; ++pass) {
+      const int s = pass * GPW + grp;
+      const int len = max(0, min(CH, cnt - s * CH));
+      const uint64_t* kp = S.keys + (tb + s) * W;
+      const V* vp = vals + tb + s;
+      A acc[4] = {A(0), A(0), A(0), A(0)};
+      unsigned cur = 0xffffffffu;  // no run yet (never a valid target: rows < 2^31)
+      auto flush = [&]() {
+        O* base;
+        if (cur & HOTF) {
+          // hot row: copy (tile mod copies) of the row's replicated partials
+          const int hc = __ldg(hot_code + (cur & ~HOTF));
+          base = hot_buf + (static_cast<long long>(hc >> 5) + (static_cast<unsigned>(t) & ((1u << (hc & 31)) - 1u))) * R;
+        } else {
+          base = out + static_cast<long long>(cur) * R;
+        }
+        merge_row<O, A, G, R>(base, acc, gl, qmask, lane, fixed_scale);
+      };
+      // loop trip count is uniform across the warp's groups except in the
+      // final partial tile; inactive groups keep their lanes converged
+      const int jmax = __reduce_max_sync(0xffffffffu, len);
+      // consume one decoded element (gathered rows g, value v, target t)
+      auto consume = [&](unsigned t, V v, const V4<F> (&gg)[NIN]) {
+        A tv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tv[q] = static_cast<A>(v) * static_cast<A>(gg[0].v[q]);
+#pragma unroll
+        for (int k = 1; k < NIN - 1; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) tv[q] *= static_cast<A>(gg[k].v[q]);
+        if (t == cur) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = fma(tv[q], static_cast<A>(gg[NIN - 1].v[q]), acc[q]);
+        } else {
+          if (cur != 0xffffffffu) flush();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = tv[q] * static_cast<A>(gg[NIN - 1].v[q]);
+          cur = t;
+        }
+      };
+      auto target = [&](const Key<W>& k) {
+        return ms_field<W>(k, fout) | (static_cast<unsigned>(k.w[W - 1] >> 32) & hotmask);
+      };
+      if constexpr (!COOP) {
+        // Broadcast loads: the G lanes of a group load the same key/value
+        // (the warp's 8 slices at step j are 8 consecutive keys: one request)
+        // and decode it redundantly with two shifts per field.  The next U
+        // elements' keys/values are loaded while the current U elements'
+        // factor rows are gathered.
+        auto run = [&](auto full_tag) {
+          constexpr bool FULL = decltype(full_tag)::value;
+          Key<W> nk[U];
+          V nv[U];
+          const uint64_t* kq = kp;
+          const V* vq = vp;
+          auto prefetch = [&](int jb) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (FULL || jb + u < len) {
+                nk[u] = load_key_stream<W>(kq, static_cast<long long>(u) * kMsSlices);
+                nv[u] = load_val_stream<V>(vq + u * kMsSlices);
+              }
+            kq += U * kMsSlices * W;
+            vq += U * kMsSlices;
+          };
+          prefetch(0);
+#pragma unroll 1
+          for (int j0 = 0; j0 < jmax; j0 += U) {
+            Key<W> kk[U];
+            V vv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) { kk[u] = nk[u]; vv[u] = nv[u]; }
+            if (FULL ? j0 + U < jmax : true) prefetch(j0 + U);
+            V4<F> g[U][NIN];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (FULL || j0 + u < len)
+#pragma unroll
+                for (int k = 0; k < NIN; ++k) g[u][k] = gather_off<F>(fin_lane[k], ms_field<W>(kk[u], fin[k]) * ROWB);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (FULL || j0 + u < len) consume(target(kk[u]), vv[u], g[u]);
+          }
+        };
+        if (cnt == T && CH % U == 0)
+          run(std::integral_constant<bool, true>{});
+        else
+          run(std::integral_constant<bool, false>{});
+      } else {
+        // Cooperative decode: lane gl < U of a group loads and decodes element
+        // j0+gl of the group's slice; the U decoded records {input row byte
+        // offsets, target, value} are broadcast within the group by shuffles.
+        Key<W> nk{};
+        V nv = V(0);
+        auto prefetch = [&](int jb) {
+          const int j = jb + gl;
+          if (gl < U && j < len) {
+            nk = load_key_stream<W>(kp, static_cast<long long>(j) * kMsSlices);
+            nv = load_val_stream<V>(vp + static_cast<long long>(j) * kMsSlices);
+          }
+        };
+        prefetch(0);
+        const int gbase = lane & ~(G - 1);
+#pragma unroll 1
+        for (int j0 = 0; j0 < jmax; j0 += U) {
+          const Key<W> kk = nk;
+          const V vv = nv;
+          prefetch(j0 + U);
+          unsigned moff[NIN];
+#pragma unroll
+          for (int k = 0; k < NIN; ++k) moff[k] = ms_field<W>(kk, fin[k]) * ROWB;
+          const unsigned mtg = (gl < U && j0 + gl < len) ? target(kk) : 0xffffffffu;
+          V4<F> g[U][NIN];
+          unsigned tg[U];
+          V vu[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            tg[u] = __shfl_sync(0xffffffffu, mtg, gbase + u);
+            vu[u] = __shfl_sync(0xffffffffu, vv, gbase + u);
+#pragma unroll
+            for (int k = 0; k < NIN; ++k) {
+              const unsigned off = __shfl_sync(0xffffffffu, moff[k], gbase + u);
+              if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], off);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (tg[u] != 0xffffffffu) consume(tg[u], vu[u], g[u]);
+        }
+      }
+      if (cur != 0xffffffffu) flush();
+    }
+  }
+}
+
+// Elements in flight per group: ~UREG registers of gathered factor data per
+// lane (cooperative decode: U <= G, one decoding lane per element).
+template <int N, int R, typename V, int UREG, bool COOP>
+constexpr int ms_u() {
+  constexpr int ub = std::max(1, UREG / ((N - 1) * 4 * static_cast<int>(sizeof(V) / 4)));
+  return COOP ? std::min(R / 4, ub) : ub;
+}
+
+template <int W, typename V, typename O, int N, int R, bool COOP = true, int MINB = 3,
+          int U = ms_u<N, R, V, (COOP ? 32 : 16), COOP>()>
+int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, cudaStream_t s) {
+  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, COOP>;
+  static int cached_bps = 0;
+  if (!cached_bps) {
+    int b = 1;
+    ALTO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kTileThreads, 0));
+    cached_bps = std::max(b, 1);
+  }
+  const long long ntiles = (P.m + S.tile - 1) / S.tile;
+  const long long need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);
+  const long long grid = std::min<long long>(need, static_cast<long long>(device_sms()) * cached_bps);
+  kern<<<static_cast<unsigned>(grid), kTileThreads, 0, s>>>(d, S, P);
+  ALTO_LAUNCH_CHECK("alto_mttkrp(mode stream)");
+  return ALTO_OK;
+}
+
+// Returns ALTO_EUNSUPPORTED (without launching) when the shape is not covered.
+template <int W, typename V, typename O>
+int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
+  if (!P.mkeys || !P.mvals || P.mtile <= 0) return ALTO_EUNSUPPORTED;
+  long long maxdim = 0;
+  for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
+  if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
+  for (int n = 0; n < d.order; ++n)
+    if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
+  const MStream S{P.mkeys, P.mvals, P.mtile, ms_fields(d, P.mode)};
+  if (!S.f.ok) return ALTO_EUNSUPPORTED;
+  if constexpr (W == 1 && sizeof(V) == 4 && sizeof(O) == 4) {
+    // tuning variants for the cfg2 shape (A/B only)
+    if (d.order == 3 && P.rank == 16) {
+      const int f = P.flags & (ALTO_STREAM_MS_COOP | ALTO_STREAM_TUNE_MINB2 | ALTO_STREAM_TUNE_U4);
+      // measured on cfg2 (ms/mode): cooperative U=4 0.61-0.63 (default), U=3
+      // 0.67-0.69, broadcast 0.70-0.72, cooperative at 2 CTAs/SM 0.75-0.79,
+      // broadcast U=4 at 2 CTAs/SM 0.73-0.77
+      if (f == ALTO_STREAM_MS_COOP) return launch_mstream<W, V, O, 3, 16, false>(d, S, P, s);
+      if (f == ALTO_STREAM_TUNE_U4) return launch_mstream<W, V, O, 3, 16, true, 3, 3>(d, S, P, s);
+    }
+  }
+  if (P.rank == 16) {
+    if (d.order == 3) return launch_mstream<W, V, O, 3, 16>(d, S, P, s);
+    if (d.order == 4) return launch_mstream<W, V, O, 4, 16>(d, S, P, s);
+    if (d.order == 5) return launch_mstream<W, V, O, 5, 16>(d, S, P, s);
+  }
+  if (P.rank == 32) {
+    if (d.order == 3) return launch_mstream<W, V, O, 3, 32>(d, S, P, s);
+    if (d.order == 4) return launch_mstream<W, V, O, 4, 32>(d, S, P, s);
+    if (d.order == 5) return launch_mstream<W, V, O, 5, 32>(d, S, P, s);
+  }
+  return ALTO_EUNSUPPORTED;
+}
+
+// out[row(s)] += sum of the row's copies (float64, fixed order), copies re-zeroed.
+// One block per hot row; thread (j, r): copies j, j + 128/R, ... of rank r.
+template <typename O>
+__global__ void __launch_bounds__(128) hot_reduce_rows_kernel(O* __restrict__ buf, const int* __restrict__ hot_rows,
+                                                              const int* __restrict__ hot_base, int R,
+                                                              O* __restrict__ out) {
+  using S = typename std::conditional<std::is_same<O, long long>::value, long long, double>::type;
+  __shared__ S s_part[128];
+  const int slot = blockIdx.x;
+  const int b0 = hot_base[slot], b1 = hot_base[slot + 1];
+  const int per = blockDim.x / R;
+  const int r = threadIdx.x % R, j = threadIdx.x / R;
+  S acc = S(0);
+  if (j < per) {
+    for (int k = b0 + j; k < b1; k += per) {
+      O* p = buf + static_cast<long long>(k) * R + r;
+      acc += static_cast<S>(*p);
+      *p = O(0);
+    }
+  }
+  s_part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    S t = S(0);
+    for (int q = 0; q < per; ++q) t += s_part[q * R + threadIdx.x];
+    O* o = out + static_cast<long long>(hot_rows[slot]) * R + threadIdx.x;
+    *o = static_cast<O>(static_cast<S>(*o) + t);
+  }
+}
+
+}  // namespace alto

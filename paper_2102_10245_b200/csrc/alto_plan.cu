@@ -2,7 +2,7 @@
 // mode-contiguous key re-encoding and the row-sorted sub-tile order (see
 // alto_fast.cuh, "planned variant").  Built once (like the reference's
 // per-mode plans and flagged copies in _make_backend, cpd.py:149-181).
-#include "alto_fast.cuh"
+#include "alto_mstream.cuh"
 
 namespace alto {
 
@@ -96,6 +96,47 @@ __global__ void subtile_order_kernel(const __grid_constant__ DevLayout L, const 
   }
 }
 
+
+// ---- per-mode stream (alto_mstream.cuh) ----------------------------------------
+// ckey = (tile << b_mode) | row, idx = element: a stable sort of these pairs is
+// the per-tile stable sort by output row.
+template <int W>
+__global__ void mstream_keys_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ packed,
+                                    long long m, int mode, int tile, uint64_t* __restrict__ ckey,
+                                    unsigned* __restrict__ idx) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m; i += stride) {
+    const unsigned row = packed_field32<W>(load_key<W>(packed, i), L.pack_off[mode], L.bits[mode]);
+    ckey[i] = (static_cast<uint64_t>(i / tile) << L.bits[mode]) | row;
+    idx[i] = static_cast<unsigned>(i);
+  }
+}
+
+template <int W, typename V>
+__global__ void mstream_scatter_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MsFields F,
+                                       const uint64_t* __restrict__ packed, const V* __restrict__ vals,
+                                       const unsigned* __restrict__ idx, long long m, int mode, int tile,
+                                       const int* __restrict__ hot_slot, uint64_t* __restrict__ skeys,
+                                       V* __restrict__ svals) {
+  const int ch = tile / kMsSlices;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < m; q += stride) {
+    const long long src = idx[q];
+    const long long t = q / tile;
+    const int p = static_cast<int>(q - t * tile);
+    const long long dst = t * tile + static_cast<long long>(p % ch) * kMsSlices + p / ch;
+    const Key<W> k = load_key<W>(packed, src);
+    Key<W> o{};
+    for (int n = 0; n < L.order; ++n) {
+      const uint64_t c = packed_field32<W>(k, L.pack_off[n], L.bits[n]);
+      o.w[W == 1 ? 0 : F.word[n]] |= c << F.sh[n];
+    }
+    if (hot_slot && hot_slot[packed_field32<W>(k, L.pack_off[mode], L.bits[mode])] >= 0) o.w[W - 1] |= 1ull << 63;
+    store_key<W>(skeys, dst, o);
+    svals[dst] = vals[src];
+  }
+}
+
 }  // namespace alto
 
 using namespace alto;
@@ -135,6 +176,70 @@ int alto_subtile_order(const alto_layout* lay, const uint64_t* packed, int64_t m
   else
     subtile_order_kernel<2><<<grid, kTileThreads, 0, s>>>(d, packed, m, mode, pos);
   ALTO_LAUNCH_CHECK("alto_subtile_order");
+  return ALTO_OK;
+}
+
+size_t alto_mode_stream_workspace_bytes(int64_t m) {
+  if (m < 0) m = 0;
+  const size_t a = (static_cast<size_t>(m) * 8 + 255) & ~size_t(255);
+  const size_t b = (static_cast<size_t>(m) * 4 + 255) & ~size_t(255);
+  return a + b + alto_sort_workspace_bytes(m, 1, 4);
+}
+
+int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,
+                     int64_t m, int32_t mode, int32_t tile, const int32_t* hot_slot, uint64_t* skeys, void* svals,
+                     void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(lay && lay->order >= 1 && lay->order <= ALTO_MAX_ORDER, "bad layout");
+  ALTO_REQUIRE(mode >= 0 && mode < lay->order, "mode out of range");
+  ALTO_REQUIRE(lay->bits[mode] <= 31, "mode stream needs mode extents below 2^31");
+  ALTO_REQUIRE(value_dtype == ALTO_F32 || value_dtype == ALTO_F64, "unsupported value dtype");
+  ALTO_REQUIRE(tile >= 256 && tile % 256 == 0, "tile must be a positive multiple of 256");
+  ALTO_REQUIRE(m >= 0 && m < (1ll << 32) - 1, "mode stream supports fewer than 2^32 elements");
+  const DevLayout d = make_dev_layout(lay);
+  const MsFields F = ms_fields(d, mode);
+  if (!F.ok) {
+    set_error("mode stream: the mode's field layout does not fit the key width");
+    return ALTO_EUNSUPPORTED;
+  }
+  const long long ntiles = (m + tile - 1) / tile;
+  int tbits = 0;
+  while ((1ll << tbits) < ntiles) ++tbits;
+  ALTO_REQUIRE(tbits + lay->bits[mode] <= 64, "too many tiles for the sort key");
+  cudaStream_t s = as_stream(stream);
+  const size_t vb = value_dtype == ALTO_F32 ? 4 : 8;
+  const size_t padded = static_cast<size_t>(ntiles) * tile;
+  if (padded > static_cast<size_t>(m)) {
+    ALTO_CUDA_TRY(cudaMemsetAsync(skeys + static_cast<size_t>(m) * d.n_words, 0,
+                                  (padded - m) * 8 * d.n_words, s));
+    ALTO_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(svals) + m * vb, 0, (padded - m) * vb, s));
+  }
+  if (m <= 0) return ALTO_OK;
+  ALTO_REQUIRE(ws && ws_bytes >= alto_mode_stream_workspace_bytes(m), "mode stream workspace too small");
+  auto* ckey = static_cast<uint64_t*>(ws);
+  const size_t a = (static_cast<size_t>(m) * 8 + 255) & ~size_t(255);
+  const size_t b = (static_cast<size_t>(m) * 4 + 255) & ~size_t(255);
+  auto* idx = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + a);
+  void* sws = static_cast<char*>(ws) + a + b;
+  const int grid = grid_for(m, 256, kSMs * 8);
+  if (d.n_words == 1)
+    mstream_keys_kernel<1><<<grid, 256, 0, s>>>(d, packed, m, mode, tile, ckey, idx);
+  else
+    mstream_keys_kernel<2><<<grid, 256, 0, s>>>(d, packed, m, mode, tile, ckey, idx);
+  ALTO_LAUNCH_CHECK("alto_mode_stream/keys");
+  const int st = alto_sort_pairs(ckey, idx, m, 1, 4, tbits + lay->bits[mode], sws,
+                                 ws_bytes - a - b, stream);
+  if (st) return st;
+  const int* hs = reinterpret_cast<const int*>(hot_slot);
+#define ALTO_MS_SCATTER(WW, VT)                                                                              \
+  mstream_scatter_kernel<WW, VT><<<grid, 256, 0, s>>>(d, F, packed, static_cast<const VT*>(values), idx, m, mode, \
+                                                      tile, hs, skeys, static_cast<VT*>(svals))
+  if (d.n_words == 1) {
+    if (vb == 4) ALTO_MS_SCATTER(1, float); else ALTO_MS_SCATTER(1, double);
+  } else {
+    if (vb == 4) ALTO_MS_SCATTER(2, float); else ALTO_MS_SCATTER(2, double);
+  }
+#undef ALTO_MS_SCATTER
+  ALTO_LAUNCH_CHECK("alto_mode_stream/scatter");
   return ALTO_OK;
 }
 

@@ -2,7 +2,7 @@
 // for the kernel design), the hot-row plan and the hot-copy reduction.
 #include <type_traits>
 
-#include "alto_fast.cuh"
+#include "alto_mstream.cuh"
 
 namespace alto {
 
@@ -10,8 +10,8 @@ namespace alto {
 // covers 32 (hot row, rank) elements x 8 copy groups: thread (g, lane) sums
 // copies g, g+8, ... of its element (coalesced across lanes), then group 0
 // adds the 8 partials in a fixed order (deterministic).
-template <typename O>
-__global__ void __launch_bounds__(256) hot_reduce_kernel(O* __restrict__ buf, const int* __restrict__ hot_rows,
+template <typename O, typename B = O>
+__global__ void __launch_bounds__(256) hot_reduce_kernel(B* __restrict__ buf, const int* __restrict__ hot_rows,
                                                          int n_hot, int copies, int R, O* __restrict__ out) {
   using S = typename std::conditional<std::is_same<O, long long>::value, long long, double>::type;
   __shared__ S s_part[8][33];
@@ -21,19 +21,19 @@ __global__ void __launch_bounds__(256) hot_reduce_kernel(O* __restrict__ buf, co
   S s = S(0);
   if (i < n) {
     // loads first, then the zeroing stores (no load-after-store chains)
-    constexpr int B = 8;
-    for (int k0 = g; k0 < copies; k0 += 8 * B) {
-      O v[B];
+    constexpr int UB = 8;
+    for (int k0 = g; k0 < copies; k0 += 8 * UB) {
+      B v[UB];
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
+      for (int u = 0; u < UB; ++u) {
         const int k = k0 + 8 * u;
-        v[u] = k < copies ? buf[k * n + i] : O(0);
+        v[u] = k < copies ? buf[k * n + i] : B(0);
       }
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
+      for (int u = 0; u < UB; ++u) {
         const int k = k0 + 8 * u;
         s += static_cast<S>(v[u]);
-        if (k < copies) buf[k * n + i] = O(0);
+        if (k < copies) buf[k * n + i] = B(0);
       }
     }
   }
@@ -46,6 +46,47 @@ __global__ void __launch_bounds__(256) hot_reduce_kernel(O* __restrict__ buf, co
     const long long h = i / R;
     O* o = out + static_cast<long long>(hot_rows[h]) * R + (i - h * R);
     *o = static_cast<O>(static_cast<S>(*o) + t);
+  }
+}
+
+// Hot-row copy plan: copies(r) = next power of two of (estimated merges of r)
+// / bound, clamped to [1, 2^max_lg]; estimated merges = min(count, ntiles) +
+// count / (tile/8) (one run per tile, plus one per slice the row spans).
+__global__ void hot_copies_kernel(const long long* __restrict__ row_ptr, const int* __restrict__ hot_rows, int n_hot,
+                                  long long ntiles, int tile, int bound, int max_lg, int* __restrict__ hot_code,
+                                  int* __restrict__ hot_base) {
+  __shared__ int s_part[1024];
+  const int per = (n_hot + blockDim.x - 1) / blockDim.x;
+  const int s0 = threadIdx.x * per, s1 = min(n_hot, s0 + per);
+  auto lg_of = [&](int s) {
+    const long long r = hot_rows[s];
+    const long long c = row_ptr[r + 1] - row_ptr[r];
+    const long long est = min(c, ntiles) + c / max(1, tile / kMsSlices);
+    const long long want = (est + bound - 1) / bound;
+    int lg = 0;
+    while (lg < max_lg && (1ll << lg) < want) ++lg;
+    return lg;
+  };
+  int sum = 0;
+  for (int s = s0; s < s1; ++s) sum += 1 << lg_of(s);
+  s_part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) {
+      const int v = s_part[i];
+      s_part[i] = run;
+      run += v;
+    }
+    hot_base[n_hot] = run;
+  }
+  __syncthreads();
+  int base = s_part[threadIdx.x];
+  for (int s = s0; s < s1; ++s) {
+    const int lg = lg_of(s);
+    hot_base[s] = base;
+    hot_code[hot_rows[s]] = (base << 5) | lg;
+    base += 1 << lg;
   }
 }
 
@@ -120,6 +161,13 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.packed = a->packed;
   P.pos = a->pos;
   P.fixed_scale = a->out_dtype == ALTO_I64 ? a->fixed_scale : nullptr;
+  P.mkeys = a->mkeys;
+  P.mvals = a->mvals;
+  P.mtile = a->mtile;
+  ALTO_REQUIRE(!a->mkeys || (a->mvals && a->mtile >= 256 && a->mtile % 256 == 0),
+               "mode stream needs values and a tile that is a multiple of 256");
+  ALTO_REQUIRE(!a->mkeys || a->n_hot <= 0 || a->hot_base, "mode-stream hot plan needs hot_base");
+  ALTO_REQUIRE(a->rank <= 128, "rank must be at most 128 for the hot-row reduction");
   Plan2 pl2{};
   P.plan2 = nullptr;
   if (a->plan) {
@@ -141,7 +189,11 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
       return ALTO_EUNSUPPORTED;
     }
     if (sti) return sti;
-    if (P.n_hot > 0) {
+    if (a->mkeys && P.n_hot > 0) {
+      hot_reduce_rows_kernel<long long><<<P.n_hot, 128, 0, s>>>(static_cast<long long*>(P.hot_buf), a->hot_rows,
+                                                                a->hot_base, a->rank, static_cast<long long*>(a->out));
+      ALTO_LAUNCH_CHECK("alto_mttkrp/hot_reduce_rows");
+    } else if (P.n_hot > 0) {
       const long long nh = static_cast<long long>(P.n_hot) * a->rank;
       hot_reduce_kernel<long long><<<static_cast<int>((nh + 31) / 32), 256, 0, s>>>(
           static_cast<long long*>(P.hot_buf), a->hot_rows, P.n_hot, P.hot_copies, a->rank,
@@ -160,7 +212,15 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
                           : (o32 ? stream_w2_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
                                  : stream_w2_f64(d, tab, P, a->value_dtype, a->factor_dtype, s));
   if (st) return st;
-  if (P.n_hot > 0) {
+  if (a->mkeys && P.n_hot > 0) {  // mode stream: per-row copy counts (alto_hot_copies)
+    if (a->out_dtype == ALTO_F32)
+      hot_reduce_rows_kernel<float><<<P.n_hot, 128, 0, s>>>(static_cast<float*>(P.hot_buf), a->hot_rows, a->hot_base,
+                                                            a->rank, static_cast<float*>(a->out));
+    else
+      hot_reduce_rows_kernel<double><<<P.n_hot, 128, 0, s>>>(static_cast<double*>(P.hot_buf), a->hot_rows,
+                                                             a->hot_base, a->rank, static_cast<double*>(a->out));
+    ALTO_LAUNCH_CHECK("alto_mttkrp/hot_reduce_rows");
+  } else if (P.n_hot > 0) {
     const long long nh = static_cast<long long>(P.n_hot) * a->rank;
     const int grid = static_cast<int>((nh + 31) / 32);
     if (a->out_dtype == ALTO_F32)
@@ -171,6 +231,18 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
                                                       static_cast<double*>(a->out));
     ALTO_LAUNCH_CHECK("alto_mttkrp/hot_reduce");
   }
+  return ALTO_OK;
+}
+
+int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_hot, int64_t m, int32_t tile,
+                    int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base, void* stream) {
+  ALTO_REQUIRE(n_hot >= 0 && tile >= 256 && bound >= 1 && max_lg >= 0 && max_lg <= 20, "bad hot copy plan arguments");
+  ALTO_REQUIRE(static_cast<long long>(n_hot) << max_lg < (1ll << 26), "too many hot-row copies");
+  if (n_hot == 0) return ALTO_OK;
+  cudaStream_t s = as_stream(stream);
+  hot_copies_kernel<<<1, 1024, 0, s>>>(reinterpret_cast<const long long*>(row_ptr), hot_rows, n_hot,
+                                       (m + tile - 1) / tile, tile, bound, max_lg, hot_code, hot_base);
+  ALTO_LAUNCH_CHECK("alto_hot_copies");
   return ALTO_OK;
 }
 

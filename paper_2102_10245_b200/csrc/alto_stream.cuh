@@ -62,6 +62,9 @@ struct StreamParams {
   const uint64_t* packed;     // mode-contiguous keys (optional, alto_pack_keys)
   const unsigned char* pos;   // per-mode sub-tile slots (optional, alto_subtile_order)
   const Plan2* plan2;         // per-mode plan words + hot-input caches (optional, host struct)
+  const uint64_t* mkeys;      // per-mode stream (optional, alto_mode_stream): keys
+  const void* mvals;          //   values
+  int mtile;                  //   tile length T
   const double* fixed_scale;  // deterministic mode: device scalar, int64 output = round(x * scale)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
 };
 

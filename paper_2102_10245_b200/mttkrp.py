@@ -179,6 +179,54 @@ def hot_plan(tensor: AltoTensor, mode: int, rank: int, out_dtype=None):
     return plan
 
 
+# Mode-stream hot plan: at most HOT_BOUND merges per replicated copy of a hot
+# row (bounds same-address contention and float32 rounding of the copies),
+# at most 2^HOT_MAX_LG copies per row.
+HOT_BOUND = 1024
+HOT_MAX_LG = 10
+
+
+def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype):
+    """Hot-row plan of the mode-stream kernel (alto_hot_copies), cached:
+    (hot_code (I_mode,) int32, hot rows, count, hot_base (count+1,) int32, zeroed copies) or None."""
+    torch = _torch()
+    key = ("hotms", mode, rank, out_dtype, MS_TILE)
+    if key in tensor._cache:
+        return tensor._cache[key]
+    hs = hot_slots(tensor, mode)
+    plan = None
+    if hs is not None:
+        _slot, rows, n = hs
+        dev = tensor.keys.device
+        _perm, ptr = row_index(tensor, mode)
+        code = torch.full((tensor.layout.dims[mode],), -1, dtype=torch.int32, device=dev)
+        base = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().alto_hot_copies(ptr.data_ptr(), rows.data_ptr(), n, tensor.nnz, MS_TILE, HOT_BOUND,
+                                               HOT_MAX_LG, code.data_ptr(), base.data_ptr(), _lib.stream_ptr()),
+                   "alto_hot_copies")
+        total = int(base[n].item())
+        buf = torch.zeros(total * rank, dtype=out_dtype, device=dev)
+        plan = (code, rows, n, base, buf)
+    tensor._cache[key] = plan
+    return plan
+
+
+def _set_hot(a, tensor: AltoTensor, mode: int, rank: int, out_dtype, ms) -> None:
+    """Fill the hot-row plan fields of an alto_mttkrp_args for the kernel that will run."""
+    if ms is not None:
+        hp = hot_plan_ms(tensor, mode, rank, out_dtype)
+        if hp is not None:
+            code, rows, n, base, buf = hp
+            a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf, a.hot_base = (
+                code.data_ptr(), rows.data_ptr(), n, 1, buf.data_ptr(), base.data_ptr())
+        return
+    hp = hot_plan(tensor, mode, rank, out_dtype)
+    if hp is not None:
+        slot, rows, n, copies, buf = hp
+        a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf = (slot.data_ptr(), rows.data_ptr(), n, copies,
+                                                                   buf.data_ptr())
+
+
 # Shared-memory budget (bytes per CTA) for the hot-input row cache.
 CACHE_BUDGET = int(__import__("os").environ.get("ALTO_CACHE_BUDGET", 32 * 1024))
 # Default planned variant: "plan2" (plan words + hot-input cache) or "pos".
@@ -235,6 +283,51 @@ def stream_plan(tensor: AltoTensor, mode: int, rank: int, fbytes: int):
     return hit
 
 
+# Per-mode stream tile length (elements); 0 disables the mode-stream kernel.
+MS_TILE = int(__import__("os").environ.get("ALTO_MS_TILE", 1024))
+
+
+def mode_stream(tensor: AltoTensor, mode: int, vals=None):
+    """Per-mode stream of the MTTKRP (alto_mode_stream), cached per (mode,
+    value dtype): the ALTO stream in tiles of MS_TILE elements, each stably
+    sorted by its `mode` coordinate, with hot-row flags.  -> (keys, values, tile)."""
+    torch = _torch()
+    vals = tensor.vals if vals is None else vals
+    key = ("mstream", mode, vals.dtype, MS_TILE)
+    hit = tensor._cache.get(key)
+    if hit is None:
+        lib = _lib.load()
+        lay = tensor.layout
+        m = tensor.nnz
+        T = MS_TILE
+        dev = tensor.keys.device
+        hs = hot_slots(tensor, mode)
+        hot = hs is not None and lay.total_bits < 64 * lay.n_words
+        ntiles = (m + T - 1) // T
+        skeys = torch.empty((max(ntiles * T, 1), lay.n_words), dtype=tensor.keys.dtype, device=dev)
+        svals = torch.empty(max(ntiles * T, 1), dtype=vals.dtype, device=dev)
+        wsb = int(lib.alto_mode_stream_workspace_bytes(m))
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals), m,
+                                  mode, T, hs[0].data_ptr() if hot else None, skeys.data_ptr(), svals.data_ptr(),
+                                  ws.data_ptr(), wsb, _lib.stream_ptr())
+        del ws
+        if rc == _lib.ALTO_EUNSUPPORTED:
+            hit = False  # field layout does not fit the key width: planned kernel instead
+        else:
+            _lib.check(rc, "alto_mode_stream")
+            hit = (skeys, svals, T)
+        tensor._cache[key] = hit
+    return hit or None
+
+
+def _use_mode_stream(tensor: AltoTensor, rank: int, fbytes: int = 4) -> bool:
+    """Mode-stream kernel: rank 16 (at rank 32 the planned kernel measured faster, cfg3)."""
+    lay = tensor.layout
+    return (MS_TILE > 0 and tensor.nnz > 0 and rank == 16 and 3 <= lay.order <= 5 and max(lay.bits) <= 31
+            and tensor.nnz < (1 << 32) - 1 and max(lay.dims) * rank * fbytes < (1 << 32))
+
+
 def packed_keys(tensor: AltoTensor):
     """Mode-contiguous re-encoding of the sorted keys (alto_pack_keys), cached."""
     torch = _torch()
@@ -287,7 +380,12 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
                                                      _lib.stream_ptr()), "alto_cast_f32_f64")
         return out
     a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
-    if planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
+    ms = (mode_stream(tensor, mode) if planned is True and PLAN_VARIANT == "pos"
+          and _use_mode_stream(tensor, rank, fdev[0].element_size()) else None)
+    if ms is not None:
+        sk, sv, st = ms
+        a.mkeys, a.mvals, a.mtile = sk.data_ptr(), sv.data_ptr(), st
+    elif planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
             and max(tensor.layout.bits) <= 31:
         a.packed = packed_keys(tensor).data_ptr()
         if planned == "pos" or (planned is True and PLAN_VARIANT == "pos"):
@@ -299,11 +397,8 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
                 a.cache_rows[i] = rws.data_ptr()
             a.cache_k = sp["k"]
             a.cache_modes = sp["modes"]
-    hp = hot_plan(tensor, mode, rank, out.dtype) if hot else None
-    if hp is not None:
-        slot, rows, n, copies, buf = hp
-        a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf = (slot.data_ptr(), rows.data_ptr(), n, copies,
-                                                                   buf.data_ptr())
+    if hot:
+        _set_hot(a, tensor, mode, rank, out.dtype, ms)
     _lib.check(_lib.load().alto_mttkrp(ctypes.byref(a), _lib.stream_ptr()), "alto_mttkrp")
     return out
 
@@ -400,13 +495,14 @@ def mttkrp_det(tensor: AltoTensor, fdev: list, mode: int, out=None):
     a, _keep = _args(tensor, fdev, mode, fixed, DEFAULT_TILE, 1, vals=vals)
     a.out_dtype = _lib.ALTO_I64
     a.fixed_scale = scale.data_ptr()
-    a.packed = packed_keys(tensor).data_ptr()
-    a.pos = subtile_order(tensor, mode).data_ptr()
-    hp = hot_plan(tensor, mode, rank, torch.int64)
-    if hp is not None:
-        slot, rows, n, copies, hbuf = hp
-        a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf = (slot.data_ptr(), rows.data_ptr(), n, copies,
-                                                                   hbuf.data_ptr())
+    ms = mode_stream(tensor, mode, vals) if _use_mode_stream(tensor, rank, fdev[0].element_size()) else None
+    if ms is not None:
+        sk, sv, st = ms
+        a.mkeys, a.mvals, a.mtile = sk.data_ptr(), sv.data_ptr(), st
+    else:
+        a.packed = packed_keys(tensor).data_ptr()
+        a.pos = subtile_order(tensor, mode).data_ptr()
+    _set_hot(a, tensor, mode, rank, torch.int64, ms)
     _lib.check(lib.alto_mttkrp(ctypes.byref(a), _lib.stream_ptr()), "alto_mttkrp(deterministic)")
     if out is None:
         out = torch.empty((dim, rank), dtype=torch.float64, device=dev)
