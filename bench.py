@@ -158,7 +158,7 @@ def run_reference(args):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json law)",
-        "config": {"workload": f"{c.name}: dims {list(c.dims)}, Zipf(1.1), rank {c.rank}; CPU sample {sample} nnz",
+        "config": {"workload": f"{c.name}: dims {list(c.dims)}, {laws_str(c)}, rank {c.rank}; CPU sample {sample} nnz",
                    "sample_nnz": sample, "threads": threads},
         "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port",
                          "sample": f"{sample} nnz of the {c.name} law, all modes, oracle port of the reference "
@@ -168,12 +168,17 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def laws_str(c) -> str:
+    """Coordinate laws of a synthetic config, e.g. 'modes: zipf(1.1), zipf(1.1), zipf(1.1)'."""
+    return "modes: " + ", ".join(f"zipf({s})" if law == "zipf" else "uniform" for law, s in c.laws)
+
+
 def traffic_from_profile(kernel_tag: str):
     """Per-launch DRAM bytes (read + write) of the dominant kernel from the
     latest committed `ncu --set full` capture of this workload (profiles/)."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_stream_kernel_ncu.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_mstream_kernel_ncu.json")))
     if not files:
         return None, None
     try:
@@ -312,11 +317,24 @@ def run_b200(args):
                          "achieved_gbs": ba / (mode_ms[n] * 1e-3) / 1e9,
                          "nnz_per_s": M / (mode_ms[n] * 1e-3)})
     tot_b = sum(p["bytes_alg"] for p in per_mode)
+    # our kernels per step: the streaming MTTKRP of each mode + its hot-row
+    # reduction when the mode has hot rows (the output zeroing is a memset)
+    mk = __import__("importlib").import_module("paper_2102_10245_b200.mttkrp")
+    ms_used = all(alto._cache.get(("mstream", n, alto.vals.dtype, mk.MS_TILE)) for n in range(N))
+    kernel_name = ("alto::mstream_kernel (alto_mstream.cuh)" if ms_used
+                   else "alto::planned_kernel (alto_fast.cuh)")
+    launches_per_step = 0
+    for n in range(N):
+        launches_per_step += 1
+        if not args.no_hot:
+            hp = (alto._cache.get(("hotms", n, R, odt, mk.MS_TILE)) if ms_used
+                  else alto._cache.get(("hot", n, R, odt)))
+            launches_per_step += 1 if hp else 0
     tot_t = sum(mode_ms) * 1e-3
     achieved = tot_b / tot_t / 1e9
     traffic, traffic_src = None, None
     if ws == 1 and nnz_total == cfg.nnz and args.config == 2 and args.out == "f32" and not args.no_hot:
-        traffic, traffic_src = traffic_from_profile("planned_kernel<1, float, float, 3, 16")
+        traffic, traffic_src = traffic_from_profile("mstream_kernel<1, float, float, 3, 16")
 
     # end-to-end through the reference-facing API: mttkrp_par with an Atomic plan
     # (the CLI protocol: prepare once, cli.py:194; per step host factors in,
@@ -378,9 +396,10 @@ def run_b200(args):
             "metric": "MTTKRP nonzeros/sec (mode-averaged)",
             "value": value, "unit": "nnz/s", "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
-            "vs_baseline": None, "dtype": "f32", "data": f"synthetic (seeded; BASELINE.json {cfg.name} law; generated on {args.gen})",
-            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, dims))}, {nnz_total} nnz, Zipf(1.1) all modes, "
-                                   f"fp32 values, rank {R}; step = MTTKRP all {N} modes",
+            "vs_baseline": None, "dtype": "f32" if vdt == torch.float32 else "f64",
+            "data": f"synthetic (seeded; BASELINE.json {cfg.name} law; generated on {args.gen})",
+            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, dims))}, {nnz_total} nnz, {laws_str(cfg)}, "
+                                   f"{cfg.values} {cfg.value_dtype} values, rank {R}; step = MTTKRP all {N} modes",
                        "nnz": nnz_total, "rank": R, "tile": args.tile, "key_bits": lay.total_bits,
                        "out_dtype": args.out, "hot_plan": not args.no_hot,
                        "l2": "flushed (256 MB write) before every timed step; keys+values "
@@ -390,13 +409,16 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "traffic": traffic, "traffic_source": traffic_src,
-                         "bytes_alg_per_launch": tot_b / N, "kernel": "alto::planned_kernel (alto_fast.cuh)",
+                         "bytes_alg_per_launch": tot_b / N,
+                         "kernel": kernel_name,
+                         "timing": "per-mode CUDA events around the whole MTTKRP call (output zeroing, "
+                                   "streaming kernel, hot-row reduction)",
                          "per_mode": per_mode},
             "e2e": {"value": N * nnz_total / (e2e_ms * 1e-3), "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "api": "paper_2102_10245_b200.mttkrp_par (Atomic plan) with pinned host fp32 factors in, "
                            "float64 result copied to pinned host memory, every mode"},
-            "gpu_launches": args.steps * N,
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clk.summary(),
             "build_ms": build_ms, "gen_s": t_gen,
             "cpals_ms_per_iter": cpals,

@@ -343,6 +343,15 @@ int alto_solve_normalize(const double* v, const double* mttkrp, int64_t rows, in
                          void* ws, size_t ws_bytes, void* stream);
 /* K13 fit terms (cpd.py:124-146): out2[0] = sum_{i,r} M[i,r] F[i,r] lambda_r,
  * out2[1] = lambda^T V_all lambda. */
+/* Fused factor update for ranks 16 / 32 (K11+K12+K10): Cholesky of V (ridge
+ * retry as alto_solve_normalize), X = M V^-1 in two streaming passes (column
+ * norms, then normalised X written as float64 and optional float32 copy),
+ * lambda = column 2-norms, and gram = X^T X of the normalised X.  mttkrp is
+ * (rows, rank) float32 or float64 (m_dtype); ALTO_EUNSUPPORTED for other
+ * ranks. */
+int alto_cpd_update(const double* v, const void* mttkrp, int32_t m_dtype, int64_t rows, int32_t rank, double* x64,
+                    float* x32, double* lambda, double* gram, int32_t* d_status, void* ws, size_t ws_bytes,
+                    void* stream);
 int alto_fit_terms(const double* mttkrp, const double* f, const double* lambda,
                    const double* v_all, int64_t rows, int32_t rank, double* out2,
                    void* ws, size_t ws_bytes, void* stream);

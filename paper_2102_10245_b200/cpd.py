@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 from .format import (AltoTensor, Strategy, apply_boundary_flags, partition,
                      plan_conflicts)
-from .mttkrp import (_check_factors, factors_to_device, mttkrp_deterministic,
+from .mttkrp import (F32_ACCUMULATE, _check_factors, factors_to_device, mttkrp_deterministic,
                      mttkrp_seq, mttkrp_stream)
 
 BACKENDS = ("seq", "oracle", "auto", "buffered", "atomic")
@@ -220,9 +220,15 @@ class DeviceBackend:
                     apply_boundary_flags(tensor, plan)  # validated like the reference; kernel ignores flag bits
                 self.engine[mode] = "stream"
 
-    def run(self, fdev: list, mode: int, out=None):
+    def run(self, fdev: list, mode: int, out=None, allow_f32: bool = False):
+        """allow_f32: the streaming engine may return its float32 result (float32
+        tensor and factors: identical to the float64 upcast the API returns)."""
+        torch = _torch()
         eng = self.engine[mode]
         if eng == "stream":
+            if (allow_f32 and out is None and F32_ACCUMULATE and self.tensor.vals.dtype == torch.float32
+                    and fdev[0].dtype == torch.float32):
+                return mttkrp_stream(self.tensor, fdev, mode, out_dtype=torch.float32)
             return mttkrp_stream(self.tensor, fdev, mode, out=out)
         if eng == "coo":
             return _coo_run(self.tensor, fdev, mode)
@@ -281,12 +287,26 @@ class DeviceCpAls:
         return self.backend.run(self.gather_factors(), mode)
 
     def update(self, mode: int):
-        """One factor update on device; no host sync."""
-        m = self.mttkrp(mode)
+        """One factor update on device; no host sync.  Ranks 16/32 use the
+        fused update (alto_cpd_update: solve, norms, normalise, Gram in two
+        streaming passes, reading a float32 MTTKRP directly); other ranks the
+        separate K11/K12/K10 kernels."""
+        torch = _torch()
+        fused = self.rank in (16, 32)
+        m = self.backend.run(self.gather_factors(), mode, allow_f32=fused)
         hadamard_device(self.grams, mode, out=self.v)
-        solve_device(self.v, m, self.ws, x64=self.f64[mode], x32=self.f32[mode] if self.use32 else None,
-                     lam=self.lam)
-        gram_device(self.f64[mode], self.ws, out=self.grams[mode])
+        if fused:
+            code = _lib.ALTO_F32 if m.dtype == torch.float32 else _lib.ALTO_F64
+            x32 = self.f32[mode] if self.use32 else None
+            _lib.check(_lib.load().alto_cpd_update(
+                self.v.data_ptr(), m.data_ptr(), code, int(m.shape[0]), self.rank, self.f64[mode].data_ptr(),
+                None if x32 is None else x32.data_ptr(), self.lam.data_ptr(), self.grams[mode].data_ptr(),
+                self.ws.status.data_ptr(), self.ws.buf.data_ptr(), self.ws.bytes, _lib.stream_ptr()),
+                "alto_cpd_update")
+        else:
+            solve_device(self.v, m, self.ws, x64=self.f64[mode], x32=self.f32[mode] if self.use32 else None,
+                         lam=self.lam)
+            gram_device(self.f64[mode], self.ws, out=self.grams[mode])
         self.m_last = m
         return m
 
@@ -295,6 +315,12 @@ class DeviceCpAls:
             _raise_singular(self.v)
 
     def fit(self, m, mode: int) -> float:
+        torch = _torch()
+        if m.dtype == torch.float32:
+            m64 = torch.empty(m.shape, dtype=torch.float64, device=m.device)
+            _lib.check(_lib.load().alto_cast_f32_f64(m.data_ptr(), m64.data_ptr(), m.numel(), _lib.stream_ptr()),
+                       "alto_cast_f32_f64")
+            m = m64
         return _device_fit(self.norm_sq, self.f64, self.grams, self.lam, m, mode, self.ws)
 
     def sweep(self) -> float:

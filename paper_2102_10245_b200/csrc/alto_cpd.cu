@@ -270,8 +270,159 @@ __global__ void cast_kernel(const double* __restrict__ in, float* __restrict__ o
     out[i] = static_cast<float>(in[i]);
 }
 
+// ---- fused factor update (K11 + K12 + K10 for ranks 16 / 32) -------------------
+// Two streaming passes over the rows of M (float32 or float64), each row
+// solved in registers against the Cholesky factor in shared memory
+// (forward + back substitution, reciprocal pivots):
+//   pass 1: column sums of squares of X = M V^-1 (per-block, fixed order);
+//   pass 2: X again, scaled by 1/lambda (zero-safe), written as float64 (and
+//           float32 gather copy) through a shared-memory tile (coalesced),
+//           plus the block's partial Gram X^T X from the same tile.
+// Rows are staged through shared memory so every global access is coalesced.
+constexpr int kUpdBlocks = 1024;
+
+template <int R>
+struct UpdCfg {
+  static constexpr int THREADS = R <= 16 ? 256 : 128;
+  static constexpr int LD = R + 1;  // padded row stride (doubles) of the tile
+};
+
+template <int R, typename MT, bool PASS2>
+__global__ void __launch_bounds__(UpdCfg<R>::THREADS) update_pass(const double* __restrict__ lmat,
+                                                                 const MT* __restrict__ mt, long long rows,
+                                                                 const double* __restrict__ lambda,
+                                                                 double* __restrict__ x64, float* __restrict__ x32,
+                                                                 const int* __restrict__ status,
+                                                                 double* __restrict__ part) {
+  constexpr int TH = UpdCfg<R>::THREADS;
+  constexpr int LD = UpdCfg<R>::LD;
+  constexpr int GPER = (R * R + TH - 1) / TH;  // Gram entries per thread
+  __shared__ double s_l[R * R];
+  __shared__ double s_rd[R];
+  __shared__ double s_scale[R];
+  __shared__ double s_t[TH * LD];
+  __shared__ double s_red[TH / 32][R];
+  if (*status == 2) return;
+  for (int i = threadIdx.x; i < R * R; i += TH) s_l[i] = lmat[i];
+  __syncthreads();
+  if (threadIdx.x < R) {
+    s_rd[threadIdx.x] = 1.0 / s_l[threadIdx.x * R + threadIdx.x];
+    if constexpr (PASS2) {
+      const double w = lambda[threadIdx.x];
+      s_scale[threadIdx.x] = w == 0.0 ? 1.0 : w;
+    }
+  }
+  __syncthreads();
+  const long long chunk = (rows + gridDim.x - 1) / gridDim.x;
+  const long long r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
+  double sq[PASS2 ? 1 : R];
+  double g[PASS2 ? GPER : 1];
+  if constexpr (!PASS2) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) sq[c] = 0.0;
+  } else {
+#pragma unroll
+    for (int q = 0; q < GPER; ++q) g[q] = 0.0;
+  }
+  for (long long base = r0; base < r1; base += TH) {
+    const int nr = static_cast<int>(min(static_cast<long long>(TH), r1 - base));
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * R; e += TH) {
+      const int r = e / R, c = e - r * R;
+      s_t[r * LD + c] = static_cast<double>(mt[base * R + e]);
+    }
+    __syncthreads();
+    double y[R];
+    // L is read through a volatile view so the compiler re-loads it (a
+    // broadcast LDS) instead of hoisting R*R doubles into registers
+    const volatile double* vl = s_l;
+    if (threadIdx.x < nr) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        double v = s_t[threadIdx.x * LD + i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) v -= vl[i * R + k] * y[k];
+        y[i] = v * s_rd[i];
+      }
+#pragma unroll
+      for (int i = R - 1; i >= 0; --i) {
+        double v = y[i];
+#pragma unroll
+        for (int k = i + 1; k < R; ++k) v -= vl[k * R + i] * y[k];
+        y[i] = v * s_rd[i];
+      }
+      if constexpr (!PASS2) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) sq[c] += y[c] * y[c];
+      }
+    }
+    if constexpr (PASS2) {
+      __syncthreads();
+      if (threadIdx.x < nr) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) s_t[threadIdx.x * LD + c] = y[c] / s_scale[c];
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < nr * R; e += TH) {
+        const int r = e / R, c = e - r * R;
+        const double v = s_t[r * LD + c];
+        x64[base * R + e] = v;
+        if (x32) x32[base * R + e] = static_cast<float>(v);
+      }
+#pragma unroll
+      for (int q = 0; q < GPER; ++q) {
+        const int idx = threadIdx.x + q * TH;
+        if (idx < R * R) {
+          const int i = idx / R, j = idx - (idx / R) * R;
+          double a = g[q];
+          for (int r = 0; r < nr; ++r) a = fma(s_t[r * LD + i], s_t[r * LD + j], a);
+          g[q] = a;
+        }
+      }
+    }
+  }
+  if constexpr (!PASS2) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      double v = sq[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) s_red[warp][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < R) {
+      double v = 0.0;
+      for (int w = 0; w < TH / 32; ++w) v += s_red[w][threadIdx.x];
+      part[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = v;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < GPER; ++q) {
+      const int idx = threadIdx.x + q * TH;
+      if (idx < R * R) part[static_cast<long long>(blockIdx.x) * R * R + idx] = g[q];
+    }
+  }
+}
+
+template <int R, typename MT>
+int update_impl(const double* v, const MT* m, long long rows, double* x64, float* x32, double* lambda, double* gram,
+                int* d_status, double* ws, cudaStream_t s) {
+  double* part = ws;
+  double* lmat = ws + static_cast<size_t>(kUpdBlocks) * R * R;
+  cholesky_kernel<<<1, 32, 0, s>>>(v, R, lmat, d_status);
+  update_pass<R, MT, false><<<kUpdBlocks, UpdCfg<R>::THREADS, 0, s>>>(lmat, m, rows, nullptr, x64, x32, d_status,
+                                                                      part);
+  lambda_kernel<<<1, 64, 0, s>>>(part, kUpdBlocks, R, lambda, d_status);
+  update_pass<R, MT, true><<<kUpdBlocks, UpdCfg<R>::THREADS, 0, s>>>(lmat, m, rows, lambda, x64, x32, d_status,
+                                                                     part);
+  sum_partials<<<1, 256, 0, s>>>(part, kUpdBlocks, R * R, gram);
+  ALTO_LAUNCH_CHECK("alto_cpd_update");
+  return ALTO_OK;
+}
+
 static size_t cpd_ws_doubles(int R) {
-  return static_cast<size_t>(kRedBlocks) * R * R + static_cast<size_t>(R) * R + 64;
+  return static_cast<size_t>(kUpdBlocks) * R * R + static_cast<size_t>(R) * R + 64;
 }
 
 }  // namespace alto
@@ -324,6 +475,28 @@ int alto_solve_normalize(const double* v, const double* mttkrp, int64_t rows, in
   normalize_kernel<<<grid_for(rows * rank, 256), 256, 0, s>>>(x64, x32, rows, rank, lambda, d_status);
   ALTO_LAUNCH_CHECK("alto_solve_normalize");
   return ALTO_OK;
+}
+
+int alto_cpd_update(const double* v, const void* mttkrp, int32_t m_dtype, int64_t rows, int32_t rank, double* x64,
+                    float* x32, double* lambda, double* gram, int32_t* d_status, void* ws, size_t ws_bytes,
+                    void* stream) {
+  ALTO_REQUIRE(m_dtype == ALTO_F32 || m_dtype == ALTO_F64, "mttkrp dtype must be float32 or float64");
+  ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
+  if (rank != 16 && rank != 32) {
+    set_error("fused factor update supports ranks 16 and 32");
+    return ALTO_EUNSUPPORTED;
+  }
+  cudaStream_t s = as_stream(stream);
+  auto* w = static_cast<double*>(ws);
+  if (rank == 16)
+    return m_dtype == ALTO_F32 ? update_impl<16>(v, static_cast<const float*>(mttkrp), rows, x64, x32, lambda, gram,
+                                                 d_status, w, s)
+                               : update_impl<16>(v, static_cast<const double*>(mttkrp), rows, x64, x32, lambda,
+                                                 gram, d_status, w, s);
+  return m_dtype == ALTO_F32 ? update_impl<32>(v, static_cast<const float*>(mttkrp), rows, x64, x32, lambda, gram,
+                                               d_status, w, s)
+                             : update_impl<32>(v, static_cast<const double*>(mttkrp), rows, x64, x32, lambda, gram,
+                                               d_status, w, s);
 }
 
 int alto_fit_terms(const double* mttkrp, const double* f, const double* lambda, const double* v_all, int64_t rows,

@@ -262,6 +262,93 @@ class TestStreamKernel:
                 a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=variant).double().cpu().numpy()
                 assert rel_error(a, b) <= 1e-6, variant
 
+    @pytest.mark.parametrize("cfg", [2, "wide", 4])
+    def test_mode_stream_layout(self, at, cfg):
+        """Per-mode stream (alto_mode_stream): each tile of T elements holds the
+        same elements as the ALTO stream's tile, stably sorted by the mode's
+        coordinate, stored as 8 interleaved slices; keys re-pack the
+        coordinates (input modes ascending, then the mode; no field straddles a
+        64-bit word) with the hot flag on the top bit."""
+        import importlib
+
+        import torch
+
+        mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+        st = synth.make_tensor(self.WIDE if cfg == "wide" else cfg, nnz=60_001)
+        dims = st.config.dims
+        alto = at.build_alto(at.CooTensor(dims, st.coords, st.values.astype(np.float64)), dtype="float32")
+        lay = alto.layout
+        W = lay.n_words
+        coords = orc.decode(orc.build_layout(dims), alto.indices)
+        vals = alto.vals.cpu().numpy()
+        T = mk.MS_TILE
+        for mode in range(len(dims)):
+            ms = mk.mode_stream(alto, mode)
+            assert ms is not None
+            sk, sv, tile = ms
+            assert tile == T
+            sk = sk.cpu().numpy().view(np.uint64).reshape(-1, W)
+            sv = sv.cpu().numpy()
+            order = [n for n in range(len(dims)) if n != mode] + [mode]
+            cur, fields = 0, {}
+            for n in order:
+                b = lay.bits[n]
+                if (cur % 64) + b > 64:
+                    cur = (cur + 63) // 64 * 64
+                fields[n] = (cur // 64, cur % 64, b)
+                cur += b
+            hs = mk.hot_slots(alto, mode)
+            hot_rows = set() if hs is None else set(hs[1][:hs[2]].cpu().numpy().tolist())
+            ch = T // 8
+            for t0 in list(range(0, alto.nnz, T))[::7] + [alto.nnz - 1 - (alto.nnz - 1) % T]:
+                cnt = min(T, alto.nnz - t0)
+                p = np.arange(cnt)
+                idx = t0 + (p % ch) * 8 + p // ch
+                keys = sk[idx]
+                dec = np.stack([(keys[:, fields[n][0]] >> np.uint64(fields[n][1])) & np.uint64((1 << fields[n][2]) - 1)
+                                for n in range(len(dims))], 1).astype(np.int64)
+                flag = (keys[:, W - 1] >> np.uint64(63)).astype(bool)
+                ref = np.argsort(coords[t0:t0 + cnt, mode], kind="stable")
+                assert np.array_equal(dec, coords[t0:t0 + cnt][ref])
+                assert np.array_equal(sv[idx], vals[t0:t0 + cnt][ref])
+                assert np.array_equal(flag, np.array([r in hot_rows for r in dec[:, mode]]))
+        rng = np.random.default_rng(4)
+        fdev = mk.factors_to_device([rng.random((d, 16)).astype(np.float32) for d in dims])
+        for mode in range(len(dims)):
+            b = mk.mttkrp_stream(alto, fdev, mode, planned=False).cpu().numpy()
+            a = mk.mttkrp_stream(alto, fdev, mode).cpu().numpy()
+            assert rel_error(a, b) <= 1e-6
+            torch.cuda.synchronize()
+
+    def test_hot_copy_plan(self, at):
+        """alto_hot_copies: per hot row 2^lg copies with 2^lg * HOT_BOUND >=
+        estimated merges (lg <= HOT_MAX_LG), laid out slot by slot."""
+        import importlib
+
+        import torch
+
+        mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+        st = synth.make_tensor(2, nnz=400_000)
+        alto = at.build_alto(at.CooTensor(st.config.dims, st.coords, st.values.astype(np.float64)), dtype="float32")
+        for mode in range(3):
+            hp = mk.hot_plan_ms(alto, mode, 16, torch.float32)
+            assert hp is not None
+            code, rows, n, base, buf = hp
+            code, rows, base = code.cpu().numpy(), rows.cpu().numpy()[:n], base.cpu().numpy()
+            counts = np.bincount(st.coords[:, mode], minlength=st.config.dims[mode])
+            ntiles = -(-alto.nnz // mk.MS_TILE)
+            assert base[0] == 0 and buf.numel() == base[n] * 16 and float(buf.abs().sum()) == 0.0
+            for s, r in enumerate(rows):
+                c = int(counts[r])
+                est = min(c, ntiles) + c // (mk.MS_TILE // 8)
+                lg = int(code[r]) & 31
+                assert code[r] >> 5 == base[s] and base[s + 1] - base[s] == 1 << lg
+                assert lg == mk.HOT_MAX_LG or (1 << lg) * mk.HOT_BOUND >= est
+                assert lg == 0 or (1 << (lg - 1)) * mk.HOT_BOUND < est
+            others = np.ones(len(code), bool)
+            others[rows] = False
+            assert (code[others] == -1).all()
+
     @pytest.mark.parametrize("cfg,rank", [(2, 16), (3, 32), ("wide", 16), (1, 16)])
     def test_deterministic_fixed_point(self, at, monkeypatch, cfg, rank):
         """Fixed-point streaming mode (used for Buffered / seq when rows are
