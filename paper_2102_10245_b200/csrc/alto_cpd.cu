@@ -283,47 +283,64 @@ constexpr int kUpdBlocks = 1024;
 
 template <int R>
 struct UpdCfg {
-  static constexpr int THREADS = R <= 16 ? 256 : 128;
+  static constexpr int THREADS = R <= 16 ? 256 : 96;  // static smem < 48 KB
+  static constexpr int MINB = R <= 16 ? 3 : 2;
   static constexpr int LD = R + 1;  // padded row stride (doubles) of the tile
 };
 
+__device__ __forceinline__ double2 lds2(const double* p) {
+  // volatile: re-loaded every use (broadcast LDS.128) rather than hoisted into registers
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
 template <int R, typename MT, bool PASS2>
-__global__ void __launch_bounds__(UpdCfg<R>::THREADS) update_pass(const double* __restrict__ lmat,
+__global__ void __launch_bounds__(UpdCfg<R>::THREADS, UpdCfg<R>::MINB) update_pass(const double* __restrict__ lmat,
                                                                  const MT* __restrict__ mt, long long rows,
                                                                  const double* __restrict__ lambda,
                                                                  double* __restrict__ x64, float* __restrict__ x32,
                                                                  const int* __restrict__ status,
                                                                  double* __restrict__ part) {
   constexpr int TH = UpdCfg<R>::THREADS;
+  constexpr int NWARP = TH / 32;
   constexpr int LD = UpdCfg<R>::LD;
-  constexpr int GPER = (R * R + TH - 1) / TH;  // Gram entries per thread
-  __shared__ double s_l[R * R];
+  constexpr int GL = R * R / 32;  // Gram entries per lane: row gi, columns gj0 .. gj0+GL-1
+  __shared__ __align__(16) double s_l[R * R];   // L, row-major
+  __shared__ __align__(16) double s_lt[R * R];  // L^T, row-major
   __shared__ double s_rd[R];
   __shared__ double s_scale[R];
   __shared__ double s_t[TH * LD];
-  __shared__ double s_red[TH / 32][R];
+  __shared__ double s_red[NWARP][R];
   if (*status == 2) return;
-  for (int i = threadIdx.x; i < R * R; i += TH) s_l[i] = lmat[i];
+  for (int i = threadIdx.x; i < R * R; i += TH) {
+    const double v = lmat[i];
+    s_l[i] = v;
+    s_lt[(i % R) * R + i / R] = v;
+  }
   __syncthreads();
   if (threadIdx.x < R) {
     s_rd[threadIdx.x] = 1.0 / s_l[threadIdx.x * R + threadIdx.x];
     if constexpr (PASS2) {
+      // reciprocal of lambda (zero-safe): one multiply per element instead of
+      // a float64 division (within 1 ulp of x / lambda)
       const double w = lambda[threadIdx.x];
-      s_scale[threadIdx.x] = w == 0.0 ? 1.0 : w;
+      s_scale[threadIdx.x] = 1.0 / (w == 0.0 ? 1.0 : w);
     }
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gi = (lane * GL) / R, gj0 = (lane * GL) % R;
   const long long chunk = (rows + gridDim.x - 1) / gridDim.x;
   const long long r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
-  double sq[PASS2 ? 1 : R];
-  double g[PASS2 ? GPER : 1];
-  if constexpr (!PASS2) {
+  // pass 1: lane owns column (lane % R) of rows phase (lane / R) of its warp's
+  // tile rows; pass 2: lane owns Gram entries (gi, gj0 .. gj0+GL-1)
+  constexpr int RPW = 32 / R;  // rows per warp step (pass 1)
+  double sq = 0.0;
+  double g[PASS2 ? GL : 1];
 #pragma unroll
-    for (int c = 0; c < R; ++c) sq[c] = 0.0;
-  } else {
-#pragma unroll
-    for (int q = 0; q < GPER; ++q) g[q] = 0.0;
-  }
+  for (int q = 0; q < (PASS2 ? GL : 1); ++q) g[q] = 0.0;
   for (long long base = r0; base < r1; base += TH) {
     const int nr = static_cast<int>(min(static_cast<long long>(TH), r1 - base));
     __syncthreads();
@@ -333,34 +350,54 @@ __global__ void __launch_bounds__(UpdCfg<R>::THREADS) update_pass(const double* 
     }
     __syncthreads();
     double y[R];
-    // L is read through a volatile view so the compiler re-loads it (a
-    // broadcast LDS) instead of hoisting R*R doubles into registers
-    const volatile double* vl = s_l;
     if (threadIdx.x < nr) {
+      // forward: L y = m (row i of L, pairs of k); back: L^T x = y (row i of L^T)
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         double v = s_t[threadIdx.x * LD + i];
 #pragma unroll
-        for (int k = 0; k < i; ++k) v -= vl[i * R + k] * y[k];
+        for (int k = 0; k + 1 < i; k += 2) {
+          const double2 l = lds2(s_l + i * R + k);
+          v -= l.x * y[k];
+          v -= l.y * y[k + 1];
+        }
+        if (i & 1) v -= s_l[i * R + i - 1] * y[i - 1];
         y[i] = v * s_rd[i];
       }
 #pragma unroll
       for (int i = R - 1; i >= 0; --i) {
         double v = y[i];
+        int k = i + 1;
+        if (k & 1) {
+          if (k < R) v -= s_lt[i * R + k] * y[k];
+          ++k;
+        }
 #pragma unroll
-        for (int k = i + 1; k < R; ++k) v -= vl[k * R + i] * y[k];
+        for (; k + 1 < R + 1 && k < R; k += 2) {
+          const double2 l = lds2(s_lt + i * R + k);
+          v -= l.x * y[k];
+          v -= l.y * y[k + 1];
+        }
         y[i] = v * s_rd[i];
       }
-      if constexpr (!PASS2) {
+    }
+    if constexpr (!PASS2) {
+      __syncthreads();
+      if (threadIdx.x < nr) {
 #pragma unroll
-        for (int c = 0; c < R; ++c) sq[c] += y[c] * y[c];
+        for (int c = 0; c < R; ++c) s_t[threadIdx.x * LD + c] = y[c];
+      }
+      __syncthreads();
+      for (int r = warp * RPW + lane / R; r < nr; r += NWARP * RPW) {
+        const double v = s_t[r * LD + (lane % R)];
+        sq = fma(v, v, sq);
       }
     }
     if constexpr (PASS2) {
       __syncthreads();
       if (threadIdx.x < nr) {
 #pragma unroll
-        for (int c = 0; c < R; ++c) s_t[threadIdx.x * LD + c] = y[c] / s_scale[c];
+        for (int c = 0; c < R; ++c) s_t[threadIdx.x * LD + c] = y[c] * s_scale[c];
       }
       __syncthreads();
       for (int e = threadIdx.x; e < nr * R; e += TH) {
@@ -369,40 +406,54 @@ __global__ void __launch_bounds__(UpdCfg<R>::THREADS) update_pass(const double* 
         x64[base * R + e] = v;
         if (x32) x32[base * R + e] = static_cast<float>(v);
       }
+      // Gram partial: warp w takes rows w, w+NWARP, ...; lane owns entries
+      // (gi, gj0 .. gj0+GL-1) of the R x R block
+      for (int r = warp; r < nr; r += NWARP) {
+        const double xi = s_t[r * LD + gi];
 #pragma unroll
-      for (int q = 0; q < GPER; ++q) {
-        const int idx = threadIdx.x + q * TH;
-        if (idx < R * R) {
-          const int i = idx / R, j = idx - (idx / R) * R;
-          double a = g[q];
-          for (int r = 0; r < nr; ++r) a = fma(s_t[r * LD + i], s_t[r * LD + j], a);
-          g[q] = a;
-        }
+        for (int q = 0; q < GL; ++q) g[q] = fma(xi, s_t[r * LD + gj0 + q], g[q]);
       }
     }
   }
   if constexpr (!PASS2) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // lanes c, c+R, ... of a warp hold column c: fixed-order fold, then warps in order
+    double v = sq;
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
-      double v = sq[c];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-      if (lane == 0) s_red[warp][c] = v;
-    }
+    for (int o = 16; o >= R; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane < R) s_red[warp][lane] = v;
     __syncthreads();
     if (threadIdx.x < R) {
-      double v = 0.0;
-      for (int w = 0; w < TH / 32; ++w) v += s_red[w][threadIdx.x];
-      part[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = v;
+      double t = 0.0;
+      for (int w = 0; w < NWARP; ++w) t += s_red[w][threadIdx.x];
+      part[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = t;
     }
   } else {
+    static_assert(NWARP * R * R <= TH * LD, "Gram reduction reuses the row tile");
+    __syncthreads();
 #pragma unroll
-    for (int q = 0; q < GPER; ++q) {
-      const int idx = threadIdx.x + q * TH;
-      if (idx < R * R) part[static_cast<long long>(blockIdx.x) * R * R + idx] = g[q];
+    for (int q = 0; q < GL; ++q) s_t[warp * R * R + gi * R + gj0 + q] = g[q];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < R * R; idx += TH) {
+      double v = 0.0;
+      for (int w = 0; w < NWARP; ++w) v += s_t[w * R * R + idx];
+      part[static_cast<long long>(blockIdx.x) * R * R + idx] = v;
     }
   }
+}
+
+// out[idx] = sum over b of part[b * width + idx], a warp per entry: lane l sums
+// blocks l, l+32, ... in order, then a fixed shuffle tree (deterministic).
+__global__ void sum_partials_warp(const double* __restrict__ part, int nblocks, int width, double* __restrict__ out,
+                                  int do_sqrt, const int* __restrict__ status) {
+  if (status && *status == 2) return;
+  const int idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (idx >= width) return;
+  double s = 0.0;
+  for (int b = lane; b < nblocks; b += 32) s += part[static_cast<long long>(b) * width + idx];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) out[idx] = do_sqrt ? sqrt(s) : s;
 }
 
 template <int R, typename MT>
@@ -413,10 +464,10 @@ int update_impl(const double* v, const MT* m, long long rows, double* x64, float
   cholesky_kernel<<<1, 32, 0, s>>>(v, R, lmat, d_status);
   update_pass<R, MT, false><<<kUpdBlocks, UpdCfg<R>::THREADS, 0, s>>>(lmat, m, rows, nullptr, x64, x32, d_status,
                                                                       part);
-  lambda_kernel<<<1, 64, 0, s>>>(part, kUpdBlocks, R, lambda, d_status);
+  sum_partials_warp<<<(R + 7) / 8, 256, 0, s>>>(part, kUpdBlocks, R, lambda, 1, d_status);
   update_pass<R, MT, true><<<kUpdBlocks, UpdCfg<R>::THREADS, 0, s>>>(lmat, m, rows, lambda, x64, x32, d_status,
                                                                      part);
-  sum_partials<<<1, 256, 0, s>>>(part, kUpdBlocks, R * R, gram);
+  sum_partials_warp<<<(R * R + 7) / 8, 256, 0, s>>>(part, kUpdBlocks, R * R, gram, 0, d_status);
   ALTO_LAUNCH_CHECK("alto_cpd_update");
   return ALTO_OK;
 }
