@@ -119,7 +119,7 @@ def cpu_baseline_sample(cfg_id: int, sample_nnz: int, threads: int, reps: int = 
         times.append(time.perf_counter() - t0)
     t = sum(times[1:]) / reps  # first rep is warm-up (cli.py:198-203 protocol)
     return {"value": len(c.dims) * sample_nnz / t, "unit": "nnz/s", "cores": threads, "kind": "port",
-            "sample": f"{sample_nnz} nnz drawn from the {c.name} law (same dims, Zipf(1.1), fp32-rounded values), "
+            "sample": f"{sample_nnz} nnz drawn from the {c.name} law (same dims, {laws_str(c)}, {c.value_dtype} values), "
                       f"all {len(c.dims)} modes, Buffered mttkrp_par over {threads} partitions/threads, "
                       f"mean of {reps} after 1 warm-up",
             "seconds_per_step": t}
@@ -251,6 +251,8 @@ def run_b200(args):
     rng = np.random.default_rng(synth.SEED_FACTOR_BASE + args.config)
     factors_host = [rng.random((d, R)).astype(fdt) for d in dims]
     fdev = factors_to_device(factors_host)
+    if args.out is None:
+        args.out = "f32" if vdt == torch.float32 else "f64"
     odt = torch.float32 if args.out == "f32" else torch.float64
     outs = [torch.empty((d, R), dtype=odt, device=dev) for d in dims]
     l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -442,7 +444,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-cpals", action="store_true")
     ap.add_argument("--no-hot", action="store_true", help="disable the hot-row plan (A/B)")
-    ap.add_argument("--out", default="f32", choices=["f32", "f64"], help="MTTKRP output dtype of the bench step")
+    ap.add_argument("--out", default=None, choices=["f32", "f64"],
+                    help="MTTKRP output dtype of the bench step (default: the config's value dtype)")
     ap.add_argument("--gen", default="device", choices=["device", "host"],
                     help="synthetic input generator: torch on the GPU (fast) or the NumPy stream of the parity tests")
     args = ap.parse_args()

@@ -273,6 +273,7 @@ int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_h
 #define ALTO_STREAM_TUNE_U4 512     /* tuning: 4 elements in flight per group (default 2) */
 #define ALTO_STREAM_MS_COOP 1024    /* tuning: mode-stream kernel with broadcast key loads instead of
                                        cooperative decode + shuffles (cfg2 shape only) */
+#define ALTO_STREAM_MS_L2_NORMAL 2048 /* tuning: mode-stream loads without the L2 evict_first policy */
 /* Ablation switches for profiling only (results are wrong when set). */
 #define ALTO_STREAM_DBG_NO_RED 8
 #define ALTO_STREAM_DBG_NO_GATHER 16

@@ -38,16 +38,31 @@ namespace alto {
 
 constexpr int kMsSlices = 8;  // slices per tile (lane groups of a rank-16 warp)
 
+// Stream loads bypass L1 and carry an L2 eviction policy (evict_first by
+// default: the stream is read once, the factor rows and output rows it
+// touches should keep the L2).
+__device__ __forceinline__ unsigned long long stream_policy(bool evict_first) {
+  unsigned long long p;
+  if (evict_first)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 template <int W>
-__device__ __forceinline__ Key<W> load_key_stream(const uint64_t* __restrict__ keys, long long i) {
+__device__ __forceinline__ Key<W> load_key_stream(const uint64_t* __restrict__ keys, long long i,
+                                                  unsigned long long pol) {
   Key<W> k;
   if constexpr (W == 1) {
     unsigned long long v;
-    asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(keys + i));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(keys + i), "l"(pol));
     k.w[0] = v;
   } else {
     unsigned long long a, b;
-    asm("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(keys + 2 * i));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+        : "=l"(a), "=l"(b)
+        : "l"(keys + 2 * i), "l"(pol));
     k.w[0] = a;
     k.w[1] = b;
   }
@@ -55,14 +70,14 @@ __device__ __forceinline__ Key<W> load_key_stream(const uint64_t* __restrict__ k
 }
 
 template <typename V>
-__device__ __forceinline__ V load_val_stream(const V* __restrict__ p) {
+__device__ __forceinline__ V load_val_stream(const V* __restrict__ p, unsigned long long pol) {
   if constexpr (sizeof(V) == 4) {
     float v;
-    asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
     return v;
   } else {
     double v;
-    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
   }
 }
@@ -154,6 +169,7 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
   const int* __restrict__ hot_code = P.n_hot > 0 ? P.hot_slot : nullptr;
   O* __restrict__ hot_buf = static_cast<O*>(P.hot_buf);
   const unsigned hotmask = hot_code ? HOTF : 0u;  // stream flags are ignored without a hot plan
+  const unsigned long long pol = stream_policy(!(P.flags & ALTO_STREAM_MS_L2_NORMAL));
 
   const long long ntiles = (P.m + T - 1) / T;
   const long long gw0 = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp;
@@ -221,8 +237,8 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
 #pragma unroll
             for (int u = 0; u < U; ++u)
               if (FULL || jb + u < len) {
-                nk[u] = load_key_stream<W>(kq, static_cast<long long>(u) * kMsSlices);
-                nv[u] = load_val_stream<V>(vq + u * kMsSlices);
+                nk[u] = load_key_stream<W>(kq, static_cast<long long>(u) * kMsSlices, pol);
+                nv[u] = load_val_stream<V>(vq + u * kMsSlices, pol);
               }
             kq += U * kMsSlices * W;
             vq += U * kMsSlices;
@@ -259,8 +275,8 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
         auto prefetch = [&](int jb) {
           const int j = jb + gl;
           if (gl < U && j < len) {
-            nk = load_key_stream<W>(kp, static_cast<long long>(j) * kMsSlices);
-            nv = load_val_stream<V>(vp + static_cast<long long>(j) * kMsSlices);
+            nk = load_key_stream<W>(kp, static_cast<long long>(j) * kMsSlices, pol);
+            nv = load_val_stream<V>(vp + static_cast<long long>(j) * kMsSlices, pol);
           }
         };
         prefetch(0);

@@ -155,3 +155,35 @@ class TestSynth:
         t = synth.make_tensor(5, nnz=5_000)
         assert t.coords.shape == (5_000, 3)
         assert len(np.unique(t.coords, axis=0)) == 5_000
+
+
+class TestBenchContract:
+    """bench.py's reference arm (CPU only) prints one JSON line with the
+    contract's keys; the argument parser accepts every documented flag."""
+
+    def test_reference_arm_runs(self):
+        import json
+        import subprocess
+        import sys
+
+        from conftest import ROOT
+
+        out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1",
+                              "--cpu-sample", "20000"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        line = json.loads(out.stdout.strip().splitlines()[-1])
+        for k in ("metric", "value", "unit", "impl", "cpu_baseline", "e2e", "config"):
+            assert k in line
+        assert line["impl"] == "reference" and line["value"] > 0
+
+    def test_flags_parse(self):
+        import subprocess
+        import sys
+
+        from conftest import ROOT
+
+        out = subprocess.run([sys.executable, "bench.py", "--help"], cwd=ROOT, capture_output=True, text=True,
+                             timeout=120)
+        assert out.returncode == 0
+        for flag in ("--gpus", "--steps", "--warmup", "--impl", "--config", "--skip-cpu", "--skip-cpals", "--out"):
+            assert flag in out.stdout
