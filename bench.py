@@ -322,14 +322,14 @@ def run_b200(args):
     # our kernels per step: the streaming MTTKRP of each mode + its hot-row
     # reduction when the mode has hot rows (the output zeroing is a memset)
     mk = __import__("importlib").import_module("paper_2102_10245_b200.mttkrp")
-    ms_used = all(alto._cache.get(("mstream", n, alto.vals.dtype, mk.MS_TILE)) for n in range(N))
+    ms_used = all(alto._cache.get(("mstream", n, alto.vals.dtype, mk.ms_tile(alto))) for n in range(N))
     kernel_name = ("alto::mstream_kernel (alto_mstream.cuh)" if ms_used
                    else "alto::planned_kernel (alto_fast.cuh)")
     launches_per_step = 0
     for n in range(N):
         launches_per_step += 1
         if not args.no_hot:
-            hp = (alto._cache.get(("hotms", n, R, odt, mk.MS_TILE)) if ms_used
+            hp = (alto._cache.get(("hotms", n, R, odt, mk.ms_tile(alto))) if ms_used
                   else alto._cache.get(("hot", n, R, odt)))
             launches_per_step += 1 if hp else 0
     tot_t = sum(mode_ms) * 1e-3

@@ -190,7 +190,8 @@ def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype):
     """Hot-row plan of the mode-stream kernel (alto_hot_copies), cached:
     (hot_code (I_mode,) int32, hot rows, count, hot_base (count+1,) int32, zeroed copies) or None."""
     torch = _torch()
-    key = ("hotms", mode, rank, out_dtype, MS_TILE)
+    T = ms_tile(tensor)
+    key = ("hotms", mode, rank, out_dtype, T)
     if key in tensor._cache:
         return tensor._cache[key]
     hs = hot_slots(tensor, mode)
@@ -201,7 +202,7 @@ def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype):
         _perm, ptr = row_index(tensor, mode)
         code = torch.full((tensor.layout.dims[mode],), -1, dtype=torch.int32, device=dev)
         base = torch.empty(n + 1, dtype=torch.int32, device=dev)
-        _lib.check(_lib.load().alto_hot_copies(ptr.data_ptr(), rows.data_ptr(), n, tensor.nnz, MS_TILE, HOT_BOUND,
+        _lib.check(_lib.load().alto_hot_copies(ptr.data_ptr(), rows.data_ptr(), n, tensor.nnz, T, HOT_BOUND,
                                                HOT_MAX_LG, code.data_ptr(), base.data_ptr(), _lib.stream_ptr()),
                    "alto_hot_copies")
         total = int(base[n].item())
@@ -287,19 +288,29 @@ def stream_plan(tensor: AltoTensor, mode: int, rank: int, fbytes: int):
 MS_TILE = int(__import__("os").environ.get("ALTO_MS_TILE", 1024))
 
 
+def ms_tile(tensor: AltoTensor) -> int:
+    """Tile length of the tensor's mode streams: MS_TILE, shrunk (to 512 or
+    256) for small tensors so that there are >= ~4 tiles per resident warp
+    (148 SMs x 24 warps)."""
+    t = MS_TILE
+    while t > 256 and tensor.nnz < 148 * 24 * 4 * t:
+        t //= 2
+    return t
+
+
 def mode_stream(tensor: AltoTensor, mode: int, vals=None):
     """Per-mode stream of the MTTKRP (alto_mode_stream), cached per (mode,
     value dtype): the ALTO stream in tiles of MS_TILE elements, each stably
     sorted by its `mode` coordinate, with hot-row flags.  -> (keys, values, tile)."""
     torch = _torch()
     vals = tensor.vals if vals is None else vals
-    key = ("mstream", mode, vals.dtype, MS_TILE)
+    T = ms_tile(tensor)
+    key = ("mstream", mode, vals.dtype, T)
     hit = tensor._cache.get(key)
     if hit is None:
         lib = _lib.load()
         lay = tensor.layout
         m = tensor.nnz
-        T = MS_TILE
         dev = tensor.keys.device
         hs = hot_slots(tensor, mode)
         hot = hs is not None and lay.total_bits < 64 * lay.n_words

@@ -281,7 +281,8 @@ class TestStreamKernel:
         W = lay.n_words
         coords = orc.decode(orc.build_layout(dims), alto.indices)
         vals = alto.vals.cpu().numpy()
-        T = mk.MS_TILE
+        T = mk.ms_tile(alto)
+        assert T == 256  # small tensor: shortest tiles
         for mode in range(len(dims)):
             ms = mk.mode_stream(alto, mode)
             assert ms is not None
@@ -336,11 +337,12 @@ class TestStreamKernel:
             code, rows, n, base, buf = hp
             code, rows, base = code.cpu().numpy(), rows.cpu().numpy()[:n], base.cpu().numpy()
             counts = np.bincount(st.coords[:, mode], minlength=st.config.dims[mode])
-            ntiles = -(-alto.nnz // mk.MS_TILE)
+            T = mk.ms_tile(alto)
+            ntiles = -(-alto.nnz // T)
             assert base[0] == 0 and buf.numel() == base[n] * 16 and float(buf.abs().sum()) == 0.0
             for s, r in enumerate(rows):
                 c = int(counts[r])
-                est = min(c, ntiles) + c // (mk.MS_TILE // 8)
+                est = min(c, ntiles) + c // (T // 8)
                 lg = int(code[r]) & 31
                 assert code[r] >> 5 == base[s] and base[s + 1] - base[s] == 1 << lg
                 assert lg == mk.HOT_MAX_LG or (1 << lg) * mk.HOT_BOUND >= est
