@@ -270,7 +270,9 @@ int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_h
                                     instead of warp-autonomous 128-element tiles */
 #define ALTO_STREAM_GENERIC 128  /* bypass the specialised (order 3-5, rank 16/32) kernels */
 #define ALTO_STREAM_TUNE_MINB2 256  /* tuning: 2 CTAs/SM launch bounds (default 3) */
-#define ALTO_STREAM_TUNE_U4 512     /* tuning: 4 elements in flight per group (default 2) */
+#define ALTO_STREAM_TUNE_U4 512     /* tuning: planned kernel: 4 elements in flight per group (default 2);
+                                       mode-stream kernel (cfg2 shape): record exchange through shared
+                                       memory instead of shuffles */
 #define ALTO_STREAM_MS_COOP 1024    /* tuning: mode-stream kernel with broadcast key loads instead of
                                        cooperative decode + shuffles (cfg2 shape only) */
 #define ALTO_STREAM_MS_L2_NORMAL 2048 /* tuning: mode-stream loads without the L2 evict_first policy */

@@ -129,7 +129,8 @@ struct MStream {
   MsFields f;
 };
 
-template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, bool COOP = false>
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, bool COOP = false,
+          bool XCH_SHFL = false>
 __global__ void __launch_bounds__(kTileThreads, MINB)
 mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStream S,
                const __grid_constant__ StreamParams P) {
@@ -142,6 +143,10 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
   constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
   constexpr unsigned HOTF = 0x80000000u;
   static_assert(!COOP || (U >= 1 && U <= G), "one decoding lane per element of a block");
+  constexpr int VW = static_cast<int>(sizeof(V) / 4);
+  constexpr int NWREC = (NIN + 1 + VW + 3) & ~3;  // record words (16-byte multiple)
+  __shared__ __align__(16) unsigned s_rec_all[COOP && !XCH_SHFL ? (kTileThreads / 32) * U * GPW * NWREC : 4];
+  unsigned* s_rec = s_rec_all + (COOP && !XCH_SHFL ? (threadIdx.x >> 5) * U * GPW * NWREC : 0);
   const int mode = P.mode;
   const int T = S.tile;
   const int CH = T / kMsSlices;
@@ -269,7 +274,10 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
       } else {
         // Cooperative decode: lane gl < U of a group loads and decodes element
         // j0+gl of the group's slice; the U decoded records {input row byte
-        // offsets, target, value} are broadcast within the group by shuffles.
+        // offsets, target, value} are broadcast within the group by shuffles
+        // (XCH_SHFL, default) or through a per-warp shared-memory block (one
+        // STS.128 per decoding lane, one broadcast LDS.128 per group and
+        // element: half the L1 wavefronts, but measured slower on cfg2).
         Key<W> nk{};
         V nv = V(0);
         auto prefetch = [&](int jb) {
@@ -293,14 +301,58 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
           V4<F> g[U][NIN];
           unsigned tg[U];
           V vu[U];
+          if constexpr (XCH_SHFL) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            tg[u] = __shfl_sync(0xffffffffu, mtg, gbase + u);
-            vu[u] = __shfl_sync(0xffffffffu, vv, gbase + u);
+            for (int u = 0; u < U; ++u) {
+              tg[u] = __shfl_sync(0xffffffffu, mtg, gbase + u);
+              vu[u] = __shfl_sync(0xffffffffu, vv, gbase + u);
 #pragma unroll
-            for (int k = 0; k < NIN; ++k) {
-              const unsigned off = __shfl_sync(0xffffffffu, moff[k], gbase + u);
-              if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], off);
+              for (int k = 0; k < NIN; ++k) {
+                const unsigned off = __shfl_sync(0xffffffffu, moff[k], gbase + u);
+                if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], off);
+              }
+            }
+          } else {
+            __syncwarp();  // previous block's records are consumed
+            if (gl < U) {
+              unsigned w[NWREC];
+#pragma unroll
+              for (int k = 0; k < NIN; ++k) w[k] = moff[k];
+              w[NIN] = mtg;
+              if constexpr (sizeof(V) == 4) {
+                w[NIN + 1] = __float_as_uint(vv);
+              } else {
+                const unsigned long long b = __double_as_longlong(vv);
+                w[NIN + 1] = static_cast<unsigned>(b);
+                w[NIN + 2] = static_cast<unsigned>(b >> 32);
+              }
+#pragma unroll
+              for (int q = NIN + 1 + VW; q < NWREC; ++q) w[q] = 0u;
+              unsigned* dst = s_rec + (gl * GPW + grp) * NWREC;
+#pragma unroll
+              for (int q = 0; q < NWREC; q += 4)
+                *reinterpret_cast<uint4*>(dst + q) = make_uint4(w[q], w[q + 1], w[q + 2], w[q + 3]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              unsigned w[NWREC];
+              const unsigned* src = s_rec + (u * GPW + grp) * NWREC;
+#pragma unroll
+              for (int q = 0; q < NWREC; q += 4) {
+                const uint4 t4 = *reinterpret_cast<const uint4*>(src + q);
+                w[q] = t4.x; w[q + 1] = t4.y; w[q + 2] = t4.z; w[q + 3] = t4.w;
+              }
+              tg[u] = w[NIN];
+              if constexpr (sizeof(V) == 4) {
+                vu[u] = __uint_as_float(w[NIN + 1]);
+              } else {
+                vu[u] = __longlong_as_double(static_cast<long long>(
+                    (static_cast<unsigned long long>(w[NIN + 2]) << 32) | w[NIN + 1]));
+              }
+#pragma unroll
+              for (int k = 0; k < NIN; ++k)
+                if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], w[k]);
             }
           }
 #pragma unroll
@@ -322,9 +374,9 @@ constexpr int ms_u() {
 }
 
 template <int W, typename V, typename O, int N, int R, bool COOP = true, int MINB = 3,
-          int U = ms_u<N, R, V, (COOP ? 32 : 16), COOP>()>
+          int U = ms_u<N, R, V, (COOP ? 32 : 16), COOP>(), bool XCH_SHFL = true>
 int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, cudaStream_t s) {
-  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, COOP>;
+  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, COOP, XCH_SHFL>;
   static int cached_bps = 0;
   if (!cached_bps) {
     int b = 1;
@@ -358,7 +410,9 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
       // 0.67-0.69, broadcast 0.70-0.72, cooperative at 2 CTAs/SM 0.75-0.79,
       // broadcast U=4 at 2 CTAs/SM 0.73-0.77
       if (f == ALTO_STREAM_MS_COOP) return launch_mstream<W, V, O, 3, 16, false>(d, S, P, s);
-      if (f == ALTO_STREAM_TUNE_U4) return launch_mstream<W, V, O, 3, 16, true, 3, 3>(d, S, P, s);
+      // shared-memory record exchange: 0.66-0.68 ms (fewer wavefronts, but
+      // the two __syncwarp per block cost more than the shuffles)
+      if (f == ALTO_STREAM_TUNE_U4) return launch_mstream<W, V, O, 3, 16, true, 3, 4, false>(d, S, P, s);
     }
   }
   if (P.rank == 16) {
