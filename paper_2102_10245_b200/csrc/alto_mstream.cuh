@@ -429,31 +429,51 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
 }
 
 // out[row(s)] += sum of the row's copies (float64, fixed order), copies re-zeroed.
-// One block per hot row; thread (j, r): copies j, j + 128/R, ... of rank r.
+// One warp per hot row; lane (j, r): rank r of copies j, j + 32/R, ... with
+// 4 independent accumulators (copies k = j + (4q + a)·32/R go to accumulator
+// a), then a fixed-order combine across accumulators and lanes.
 template <typename O>
-__global__ void __launch_bounds__(128) hot_reduce_rows_kernel(O* __restrict__ buf, const int* __restrict__ hot_rows,
-                                                              const int* __restrict__ hot_base, int R,
+__global__ void __launch_bounds__(256) hot_reduce_rows_kernel(O* __restrict__ buf, const int* __restrict__ hot_rows,
+                                                              const int* __restrict__ hot_base, int n_hot, int R,
                                                               O* __restrict__ out) {
   using S = typename std::conditional<std::is_same<O, long long>::value, long long, double>::type;
-  __shared__ S s_part[128];
-  const int slot = blockIdx.x;
+  const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (slot >= n_hot) return;
+  const int lane = threadIdx.x & 31;
+  const int per = R >= 32 ? 1 : 32 / R;
+  const int r = lane % R, j = lane / R;
+  const bool active = R >= 32 ? (lane < R) : (j < per);
   const int b0 = hot_base[slot], b1 = hot_base[slot + 1];
-  const int per = blockDim.x / R;
-  const int r = threadIdx.x % R, j = threadIdx.x / R;
-  S acc = S(0);
-  if (j < per) {
-    for (int k = b0 + j; k < b1; k += per) {
+  S acc[4] = {S(0), S(0), S(0), S(0)};
+  if (active) {
+    int k = b0 + j;
+    for (; k + 3 * per < b1; k += 4 * per) {
       O* p = buf + static_cast<long long>(k) * R + r;
-      acc += static_cast<S>(*p);
+      const long long st = static_cast<long long>(per) * R;
+      const O v0 = p[0], v1 = p[st], v2 = p[2 * st], v3 = p[3 * st];
+      acc[0] += static_cast<S>(v0);
+      acc[1] += static_cast<S>(v1);
+      acc[2] += static_cast<S>(v2);
+      acc[3] += static_cast<S>(v3);
+      p[0] = O(0);
+      p[st] = O(0);
+      p[2 * st] = O(0);
+      p[3 * st] = O(0);
+    }
+    for (int a = 0; k < b1; k += per, ++a) {
+      O* p = buf + static_cast<long long>(k) * R + r;
+      acc[a] += static_cast<S>(*p);
       *p = O(0);
     }
   }
-  s_part[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x < R) {
-    S t = S(0);
-    for (int q = 0; q < per; ++q) t += s_part[q * R + threadIdx.x];
-    O* o = out + static_cast<long long>(hot_rows[slot]) * R + threadIdx.x;
+  S t = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  // lanes r, r+R, ... hold rank r: fold in a fixed order
+  for (int o = 16; o >= R && o > 0; o >>= 1) {
+    const S u = __shfl_down_sync(0xffffffffu, t, o);
+    t += u;
+  }
+  if (lane < R) {
+    O* o = out + static_cast<long long>(hot_rows[slot]) * R + lane;
     *o = static_cast<O>(static_cast<S>(*o) + t);
   }
 }

@@ -167,7 +167,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   ALTO_REQUIRE(!a->mkeys || (a->mvals && a->mtile >= 256 && a->mtile % 256 == 0),
                "mode stream needs values and a tile that is a multiple of 256");
   ALTO_REQUIRE(!a->mkeys || a->n_hot <= 0 || a->hot_base, "mode-stream hot plan needs hot_base");
-  ALTO_REQUIRE(a->rank <= 128, "rank must be at most 128 for the hot-row reduction");
+  ALTO_REQUIRE(!a->mkeys || a->rank <= 32, "the mode-stream hot-row reduction supports ranks up to 32");
   Plan2 pl2{};
   P.plan2 = nullptr;
   if (a->plan) {
@@ -190,8 +190,9 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
     }
     if (sti) return sti;
     if (a->mkeys && P.n_hot > 0) {
-      hot_reduce_rows_kernel<long long><<<P.n_hot, 128, 0, s>>>(static_cast<long long*>(P.hot_buf), a->hot_rows,
-                                                                a->hot_base, a->rank, static_cast<long long*>(a->out));
+      hot_reduce_rows_kernel<long long><<<(P.n_hot + 7) / 8, 256, 0, s>>>(
+          static_cast<long long*>(P.hot_buf), a->hot_rows, a->hot_base, P.n_hot, a->rank,
+          static_cast<long long*>(a->out));
       ALTO_LAUNCH_CHECK("alto_mttkrp/hot_reduce_rows");
     } else if (P.n_hot > 0) {
       const long long nh = static_cast<long long>(P.n_hot) * a->rank;
@@ -214,11 +215,13 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   if (st) return st;
   if (a->mkeys && P.n_hot > 0) {  // mode stream: per-row copy counts (alto_hot_copies)
     if (a->out_dtype == ALTO_F32)
-      hot_reduce_rows_kernel<float><<<P.n_hot, 128, 0, s>>>(static_cast<float*>(P.hot_buf), a->hot_rows, a->hot_base,
-                                                            a->rank, static_cast<float*>(a->out));
+      hot_reduce_rows_kernel<float><<<(P.n_hot + 7) / 8, 256, 0, s>>>(static_cast<float*>(P.hot_buf), a->hot_rows,
+                                                                      a->hot_base, P.n_hot, a->rank,
+                                                                      static_cast<float*>(a->out));
     else
-      hot_reduce_rows_kernel<double><<<P.n_hot, 128, 0, s>>>(static_cast<double*>(P.hot_buf), a->hot_rows,
-                                                             a->hot_base, a->rank, static_cast<double*>(a->out));
+      hot_reduce_rows_kernel<double><<<(P.n_hot + 7) / 8, 256, 0, s>>>(static_cast<double*>(P.hot_buf), a->hot_rows,
+                                                                       a->hot_base, P.n_hot, a->rank,
+                                                                       static_cast<double*>(a->out));
     ALTO_LAUNCH_CHECK("alto_mttkrp/hot_reduce_rows");
   } else if (P.n_hot > 0) {
     const long long nh = static_cast<long long>(P.n_hot) * a->rank;
