@@ -263,6 +263,17 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
 int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_hot, int64_t m, int32_t tile,
                     int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base, void* stream);
 
+/* COO coalesce on the device (coo.py:97-114): rows sorted lexicographically
+ * with mode 0 as the primary key (stable), duplicates summed in float64 in
+ * that order from 0.0 (bitwise equal to the reference's np.bincount).
+ * coords (m, order) int64 row-major, values (m,) float64; bits[n] =
+ * bits_for(I_n) (host array, sum <= 128); out_coords / out_values hold up to
+ * m rows; *d_count (device int64) receives the number of distinct rows. */
+size_t alto_coalesce_workspace_bytes(int64_t m, int32_t n_words);
+int alto_coalesce(const int64_t* coords, const double* values, int64_t m, int32_t order, const int32_t* bits,
+                  int64_t* out_coords, double* out_values, int64_t* d_count, void* ws, size_t ws_bytes,
+                  void* stream);
+
 /* Streaming-kernel tuning switches (alto_mttkrp_args.flags). */
 #define ALTO_STREAM_WARP_AGG 1   /* warp-aggregate in-tile sort atomics */
 #define ALTO_STREAM_FULL_BINS 2  /* scan all sort bins instead of the tile span */

@@ -366,3 +366,19 @@ def rel_error(out, ref) -> float:
     d = float(np.linalg.norm(ref))
     e = float(np.linalg.norm(np.asarray(out) - ref))
     return e / d if d else e
+
+
+def coalesce(coords, values):
+    """COO coalesce (pkg/src/altotensor/coo.py:97-114): stable lexicographic
+    row order with mode 0 primary, duplicates summed by np.bincount (i.e.
+    sequentially in that order from 0.0).  -> (coords, values)."""
+    c = np.ascontiguousarray(coords, dtype=np.int64)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if c.shape[0] == 0:
+        return c, v
+    perm = np.lexsort(tuple(c[:, n] for n in range(c.shape[1] - 1, -1, -1)))
+    c, v = c[perm], v[perm]
+    new = np.ones(c.shape[0], dtype=bool)
+    new[1:] = (c[1:] != c[:-1]).any(axis=1)
+    return c[new], np.bincount(np.cumsum(new) - 1, weights=v)
+

@@ -94,6 +94,9 @@ SIGNATURES = [
     ("alto_pack_keys", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     ("alto_subtile_order", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_mode_stream_workspace_bytes", c_size_t, [c_int64]),
+    ("alto_coalesce_workspace_bytes", c_size_t, [c_int64, c_int32]),
+    ("alto_coalesce", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_size_t, c_void_p]),
     ("alto_cpd_update", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_hot_copies", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p,
