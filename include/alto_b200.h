@@ -361,11 +361,14 @@ int alto_solve_normalize(const double* v, const double* mttkrp, int64_t rows, in
  * retry as alto_solve_normalize), X = M V^-1 in two streaming passes (column
  * norms, then normalised X written as float64 and optional float32 copy),
  * lambda = column 2-norms, and gram = X^T X of the normalised X.  mttkrp is
- * (rows, rank) float32 or float64 (m_dtype); ALTO_EUNSUPPORTED for other
- * ranks. */
+ * (rows, rank) float32 or float64 (m_dtype).  Rank 16 runs X = M W
+ * (W = V^-1) and the Gram on the float64 tensor cores (mma.sync m8n8k4);
+ * flags & ALTO_CPD_SCALAR selects the scalar substitution kernels (rank 32
+ * always uses them).  ALTO_EUNSUPPORTED for other ranks. */
+#define ALTO_CPD_SCALAR 1
 int alto_cpd_update(const double* v, const void* mttkrp, int32_t m_dtype, int64_t rows, int32_t rank, double* x64,
-                    float* x32, double* lambda, double* gram, int32_t* d_status, void* ws, size_t ws_bytes,
-                    void* stream);
+                    float* x32, double* lambda, double* gram, int32_t* d_status, int32_t flags, void* ws,
+                    size_t ws_bytes, void* stream);
 int alto_fit_terms(const double* mttkrp, const double* f, const double* lambda,
                    const double* v_all, int64_t rows, int32_t rank, double* out2,
                    void* ws, size_t ws_bytes, void* stream);

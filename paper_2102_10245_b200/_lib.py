@@ -98,7 +98,7 @@ SIGNATURES = [
     ("alto_coalesce", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_size_t, c_void_p]),
     ("alto_cpd_update", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p,
-                                  c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+                                  c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
     ("alto_hot_copies", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p,
                                   c_void_p]),
     ("alto_mode_stream", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32,

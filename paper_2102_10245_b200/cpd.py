@@ -24,6 +24,8 @@ from .mttkrp import (F32_ACCUMULATE, _check_factors, factors_to_device, mttkrp_d
                      mttkrp_seq, mttkrp_stream)
 
 BACKENDS = ("seq", "oracle", "auto", "buffered", "atomic")
+# alto_cpd_update flags (ALTO_CPD_SCALAR = 1: scalar substitution instead of the rank-16 DMMA path)
+CPD_UPDATE_FLAGS = int(__import__("os").environ.get("ALTO_CPD_FLAGS", "0"))
 
 
 def _torch():
@@ -301,8 +303,8 @@ class DeviceCpAls:
             _lib.check(_lib.load().alto_cpd_update(
                 self.v.data_ptr(), m.data_ptr(), code, int(m.shape[0]), self.rank, self.f64[mode].data_ptr(),
                 None if x32 is None else x32.data_ptr(), self.lam.data_ptr(), self.grams[mode].data_ptr(),
-                self.ws.status.data_ptr(), self.ws.buf.data_ptr(), self.ws.bytes, _lib.stream_ptr()),
-                "alto_cpd_update")
+                self.ws.status.data_ptr(), CPD_UPDATE_FLAGS, self.ws.buf.data_ptr(), self.ws.bytes,
+                _lib.stream_ptr()), "alto_cpd_update")
         else:
             solve_device(self.v, m, self.ws, x64=self.f64[mode], x32=self.f32[mode] if self.use32 else None,
                          lam=self.lam)

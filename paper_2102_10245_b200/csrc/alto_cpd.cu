@@ -456,6 +456,189 @@ __global__ void sum_partials_warp(const double* __restrict__ part, int nblocks, 
   if (lane == 0) out[idx] = do_sqrt ? sqrt(s) : s;
 }
 
+// ---- rank-16 update on the float64 tensor cores (DMMA m8n8k4) ------------------
+// X = M W (W = V^-1 from the Cholesky factor) and the Gram X^T X are
+// GEMM-shaped, so rank 16 runs them as mma.sync m8n8k4 f64 (exact float64
+// products and sums, like the scalar path up to summation order).  A warp
+// takes 8 rows at a time: each lane loads 4 consecutive entries of its row
+// (row = lane/4, columns 4*(lane%4) .. +3: one coalesced 16-byte load) and
+// uses entry ks in k-step ks, so MMA k-index t stands for column 4t+ks; the
+// W fragments are permuted the same way and stay in registers.  Pass 1 sums
+// the squares of X per column; pass 2 scales by 1/lambda, writes X (float64
+// + float32 copy) and accumulates X^T X from a per-warp 8x16 shared tile.
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+constexpr int kTcThreads = 256;
+
+template <typename MT, bool PASS2>
+__global__ void __launch_bounds__(kTcThreads) update16_tc(const double* __restrict__ w, const MT* __restrict__ mt,
+                                                          long long rows, const double* __restrict__ lambda,
+                                                          double* __restrict__ x64, float* __restrict__ x32,
+                                                          const int* __restrict__ status,
+                                                          double* __restrict__ part) {
+  constexpr int R = 16;
+  constexpr int NW = kTcThreads / 32;
+  __shared__ double s_x[NW][8][R + 1];
+  __shared__ double s_red[NW][R * R];
+  if (*status == 2) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  // B fragments of W: k-step ks, n-tile nt: W[4*tig + ks][8*nt + gid]
+  double bw[4][2];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) bw[ks][nt] = w[(4 * tig + ks) * R + 8 * nt + gid];
+  double rl[2][2];  // 1/lambda of this lane's output columns 8*nt + 2*tig + {0,1}
+  if constexpr (PASS2) {
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double l = lambda[8 * nt + 2 * tig + q];
+        rl[nt][q] = 1.0 / (l == 0.0 ? 1.0 : l);
+      }
+  }
+  double sq[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  double g[2][2][2] = {};  // Gram tile (mt, nt), fragment entries
+  const long long groups = (rows + 7) / 8;
+  const long long gpb = (groups + gridDim.x - 1) / gridDim.x;  // 8-row groups per block (contiguous)
+  const long long g0 = blockIdx.x * gpb, g1 = min(groups, g0 + gpb);
+  for (long long grp = g0 + warp; grp < g1; grp += NW) {
+    const long long row = grp * 8 + gid;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (row < rows) {
+      if constexpr (sizeof(MT) == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(mt + row * R) + tig);
+        a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+      } else {
+        const double2 v0 = __ldg(reinterpret_cast<const double2*>(mt + row * R) + 2 * tig);
+        const double2 v1 = __ldg(reinterpret_cast<const double2*>(mt + row * R) + 2 * tig + 1);
+        a[0] = v0.x; a[1] = v0.y; a[2] = v1.x; a[3] = v1.y;
+      }
+    }
+    double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // X[gid][8*nt + 2*tig + q]
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma(c[nt], a[ks], bw[ks][nt]);
+    if constexpr (!PASS2) {
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) sq[nt][q] = fma(c[nt][q], c[nt][q], sq[nt][q]);
+    } else {
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) c[nt][q] = row < rows ? c[nt][q] * rl[nt][q] : 0.0;
+      if (row < rows) {
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          *reinterpret_cast<double2*>(x64 + row * R + 8 * nt + 2 * tig) = make_double2(c[nt][0], c[nt][1]);
+          if (x32)
+            *reinterpret_cast<float2*>(x32 + row * R + 8 * nt + 2 * tig) =
+                make_float2(static_cast<float>(c[nt][0]), static_cast<float>(c[nt][1]));
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) s_x[warp][gid][8 * nt + 2 * tig + q] = c[nt][q];
+      __syncwarp();
+      // G(mt, nt) += X[:, 8mt..]^T X[:, 8nt..] over the 8 rows (2 k-steps of 4)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        double fa[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) fa[t] = s_x[warp][4 * ks + tig][8 * t + gid];
+#pragma unroll
+        for (int mt2 = 0; mt2 < 2; ++mt2)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) dmma(g[mt2][nt], fa[mt2], fa[nt]);
+      }
+    }
+  }
+  if constexpr (!PASS2) {
+    // column (8nt + 2tig + q) partials live in lanes with the same tig: fold gid
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        double v = sq[nt][q];
+#pragma unroll
+        for (int o = 16; o >= 4; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (gid == 0) s_red[warp][8 * nt + 2 * tig + q] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < R) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < NW; ++w2) t += s_red[w2][threadIdx.x];
+      part[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = t;
+    }
+  } else {
+#pragma unroll
+    for (int mt2 = 0; mt2 < 2; ++mt2)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) s_red[warp][(8 * mt2 + gid) * R + 8 * nt + 2 * tig + q] = g[mt2][nt][q];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < R * R; idx += kTcThreads) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < NW; ++w2) t += s_red[w2][idx];
+      part[static_cast<long long>(blockIdx.x) * R * R + idx] = t;
+    }
+  }
+}
+
+// W = V^-1 = L^-T L^-1 from the Cholesky factor: one warp, lane j solves
+// column j of L^-1 (forward substitution), then W = Z^T Z.
+__global__ void inverse16_kernel(const double* __restrict__ lmat, double* __restrict__ w,
+                                 const int* __restrict__ status) {
+  constexpr int R = 16;
+  __shared__ double s_z[R][R + 1];  // L^-1, row-major
+  if (*status == 2) return;
+  const int j = threadIdx.x;
+  if (j < R) {
+    for (int i = 0; i < R; ++i) {
+      double v = i == j ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) v -= lmat[i * R + k] * s_z[k][j];
+      s_z[i][j] = i < j ? 0.0 : v / lmat[i * R + i];
+    }
+  }
+  __syncwarp();
+  for (int idx = threadIdx.x; idx < R * R; idx += 32) {
+    const int r = idx / R, c = idx % R;
+    double v = 0.0;
+    for (int k = (r > c ? r : c); k < R; ++k) v += s_z[k][r] * s_z[k][c];
+    w[idx] = v;
+  }
+}
+
+template <typename MT>
+int update16_tc_impl(const double* v, const MT* m, long long rows, double* x64, float* x32, double* lambda,
+                     double* gram, int* d_status, double* ws, cudaStream_t s) {
+  constexpr int R = 16;
+  double* part = ws;
+  double* lmat = ws + static_cast<size_t>(kUpdBlocks) * R * R;
+  double* winv = lmat + R * R;
+  cholesky_kernel<<<1, 32, 0, s>>>(v, R, lmat, d_status);
+  inverse16_kernel<<<1, 32, 0, s>>>(lmat, winv, d_status);
+  update16_tc<MT, false><<<kUpdBlocks, kTcThreads, 0, s>>>(winv, m, rows, nullptr, x64, x32, d_status, part);
+  sum_partials_warp<<<(R + 7) / 8, 256, 0, s>>>(part, kUpdBlocks, R, lambda, 1, d_status);
+  update16_tc<MT, true><<<kUpdBlocks, kTcThreads, 0, s>>>(winv, m, rows, lambda, x64, x32, d_status, part);
+  sum_partials_warp<<<(R * R + 7) / 8, 256, 0, s>>>(part, kUpdBlocks, R * R, gram, 0, d_status);
+  ALTO_LAUNCH_CHECK("alto_cpd_update(tc)");
+  return ALTO_OK;
+}
+
 template <int R, typename MT>
 int update_impl(const double* v, const MT* m, long long rows, double* x64, float* x32, double* lambda, double* gram,
                 int* d_status, double* ws, cudaStream_t s) {
@@ -473,7 +656,7 @@ int update_impl(const double* v, const MT* m, long long rows, double* x64, float
 }
 
 static size_t cpd_ws_doubles(int R) {
-  return static_cast<size_t>(kUpdBlocks) * R * R + static_cast<size_t>(R) * R + 64;
+  return static_cast<size_t>(kUpdBlocks) * R * R + 2 * static_cast<size_t>(R) * R + 64;
 }
 
 }  // namespace alto
@@ -529,8 +712,8 @@ int alto_solve_normalize(const double* v, const double* mttkrp, int64_t rows, in
 }
 
 int alto_cpd_update(const double* v, const void* mttkrp, int32_t m_dtype, int64_t rows, int32_t rank, double* x64,
-                    float* x32, double* lambda, double* gram, int32_t* d_status, void* ws, size_t ws_bytes,
-                    void* stream) {
+                    float* x32, double* lambda, double* gram, int32_t* d_status, int32_t flags, void* ws,
+                    size_t ws_bytes, void* stream) {
   ALTO_REQUIRE(m_dtype == ALTO_F32 || m_dtype == ALTO_F64, "mttkrp dtype must be float32 or float64");
   ALTO_REQUIRE(ws && ws_bytes >= alto_cpd_workspace_bytes(rank), "cpd workspace too small");
   if (rank != 16 && rank != 32) {
@@ -539,6 +722,12 @@ int alto_cpd_update(const double* v, const void* mttkrp, int32_t m_dtype, int64_
   }
   cudaStream_t s = as_stream(stream);
   auto* w = static_cast<double*>(ws);
+  const bool scalar = (flags & 1) != 0;  // ALTO_CPD_SCALAR: substitution kernels instead of DMMA
+  if (rank == 16 && !scalar)
+    return m_dtype == ALTO_F32 ? update16_tc_impl(v, static_cast<const float*>(mttkrp), rows, x64, x32, lambda, gram,
+                                                  d_status, w, s)
+                               : update16_tc_impl(v, static_cast<const double*>(mttkrp), rows, x64, x32, lambda,
+                                                  gram, d_status, w, s);
   if (rank == 16)
     return m_dtype == ALTO_F32 ? update_impl<16>(v, static_cast<const float*>(mttkrp), rows, x64, x32, lambda, gram,
                                                  d_status, w, s)
