@@ -475,71 +475,79 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 constexpr int kTcThreads = 256;
 
-template <typename MT, bool PASS2>
-__global__ void __launch_bounds__(kTcThreads) update16_tc(const double* __restrict__ w, const MT* __restrict__ mt,
-                                                          long long rows, const double* __restrict__ lambda,
-                                                          double* __restrict__ x64, float* __restrict__ x32,
-                                                          const int* __restrict__ status,
-                                                          double* __restrict__ part) {
-  constexpr int R = 16;
+template <int R, typename MT, bool PASS2>
+__global__ void __launch_bounds__(kTcThreads) update_tc(const double* __restrict__ w, const MT* __restrict__ mt,
+                                                        long long rows, const double* __restrict__ lambda,
+                                                        double* __restrict__ x64, float* __restrict__ x32,
+                                                        const int* __restrict__ status, double* __restrict__ part) {
+  constexpr int KS = R / 4;  // k-steps: a lane holds KS consecutive entries of its row
+  constexpr int NT = R / 8;  // 8-column tiles
   constexpr int NW = kTcThreads / 32;
+  constexpr int PER = R * R / kTcThreads;  // Gram entries summed per thread at the end
   __shared__ double s_x[NW][8][R + 1];
-  __shared__ double s_red[NW][R * R];
+  __shared__ double s_red[R * R];
   if (*status == 2) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gid = lane >> 2, tig = lane & 3;
-  // B fragments of W: k-step ks, n-tile nt: W[4*tig + ks][8*nt + gid]
-  double bw[4][2];
+  // B fragments of W: k-step ks, n-tile nt: W[KS*tig + ks][8*nt + gid]
+  double bw[KS][NT];
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks)
+  for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) bw[ks][nt] = w[(4 * tig + ks) * R + 8 * nt + gid];
-  double rl[2][2];  // 1/lambda of this lane's output columns 8*nt + 2*tig + {0,1}
+    for (int nt = 0; nt < NT; ++nt) bw[ks][nt] = w[(KS * tig + ks) * R + 8 * nt + gid];
+  double rl[NT][2];  // 1/lambda of this lane's output columns 8*nt + 2*tig + {0,1}
   if constexpr (PASS2) {
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const double l = lambda[8 * nt + 2 * tig + q];
         rl[nt][q] = 1.0 / (l == 0.0 ? 1.0 : l);
       }
   }
-  double sq[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  double g[2][2][2] = {};  // Gram tile (mt, nt), fragment entries
+  double sq[NT][2] = {};
+  double g[PASS2 ? NT : 1][PASS2 ? NT : 1][2] = {};  // Gram tile (mt, nt), fragment entries
   const long long groups = (rows + 7) / 8;
   const long long gpb = (groups + gridDim.x - 1) / gridDim.x;  // 8-row groups per block (contiguous)
   const long long g0 = blockIdx.x * gpb, g1 = min(groups, g0 + gpb);
   for (long long grp = g0 + warp; grp < g1; grp += NW) {
     const long long row = grp * 8 + gid;
-    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    double a[KS];
+#pragma unroll
+    for (int q = 0; q < KS; ++q) a[q] = 0.0;
     if (row < rows) {
       if constexpr (sizeof(MT) == 4) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(mt + row * R) + tig);
-        a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+#pragma unroll
+        for (int q = 0; q < KS; q += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(mt + row * R + KS * tig + q));
+          a[q] = v.x; a[q + 1] = v.y; a[q + 2] = v.z; a[q + 3] = v.w;
+        }
       } else {
-        const double2 v0 = __ldg(reinterpret_cast<const double2*>(mt + row * R) + 2 * tig);
-        const double2 v1 = __ldg(reinterpret_cast<const double2*>(mt + row * R) + 2 * tig + 1);
-        a[0] = v0.x; a[1] = v0.y; a[2] = v1.x; a[3] = v1.y;
+#pragma unroll
+        for (int q = 0; q < KS; q += 2) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(mt + row * R + KS * tig + q));
+          a[q] = v.x; a[q + 1] = v.y;
+        }
       }
     }
-    double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // X[gid][8*nt + 2*tig + q]
+    double c[NT][2] = {};  // X[gid][8*nt + 2*tig + q]
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
+    for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) dmma(c[nt], a[ks], bw[ks][nt]);
+      for (int nt = 0; nt < NT; ++nt) dmma(c[nt], a[ks], bw[ks][nt]);
     if constexpr (!PASS2) {
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int q = 0; q < 2; ++q) sq[nt][q] = fma(c[nt][q], c[nt][q], sq[nt][q]);
     } else {
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int q = 0; q < 2; ++q) c[nt][q] = row < rows ? c[nt][q] * rl[nt][q] : 0.0;
       if (row < rows) {
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
+        for (int nt = 0; nt < NT; ++nt) {
           *reinterpret_cast<double2*>(x64 + row * R + 8 * nt + 2 * tig) = make_double2(c[nt][0], c[nt][1]);
           if (x32)
             *reinterpret_cast<float2*>(x32 + row * R + 8 * nt + 2 * tig) =
@@ -548,61 +556,69 @@ __global__ void __launch_bounds__(kTcThreads) update16_tc(const double* __restri
       }
       __syncwarp();
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int q = 0; q < 2; ++q) s_x[warp][gid][8 * nt + 2 * tig + q] = c[nt][q];
       __syncwarp();
       // G(mt, nt) += X[:, 8mt..]^T X[:, 8nt..] over the 8 rows (2 k-steps of 4)
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
-        double fa[2];
+        double fa[NT];
 #pragma unroll
-        for (int t = 0; t < 2; ++t) fa[t] = s_x[warp][4 * ks + tig][8 * t + gid];
+        for (int t = 0; t < NT; ++t) fa[t] = s_x[warp][4 * ks + tig][8 * t + gid];
 #pragma unroll
-        for (int mt2 = 0; mt2 < 2; ++mt2)
+        for (int mt2 = 0; mt2 < NT; ++mt2)
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt) dmma(g[mt2][nt], fa[mt2], fa[nt]);
+          for (int nt = 0; nt < NT; ++nt) dmma(g[mt2][nt], fa[mt2], fa[nt]);
       }
     }
   }
   if constexpr (!PASS2) {
     // column (8nt + 2tig + q) partials live in lanes with the same tig: fold gid
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         double v = sq[nt][q];
 #pragma unroll
         for (int o = 16; o >= 4; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (gid == 0) s_red[warp][8 * nt + 2 * tig + q] = v;
+        if (gid == 0) s_x[warp][0][8 * nt + 2 * tig + q] = v;
       }
     __syncthreads();
     if (threadIdx.x < R) {
       double t = 0.0;
-      for (int w2 = 0; w2 < NW; ++w2) t += s_red[w2][threadIdx.x];
+      for (int w2 = 0; w2 < NW; ++w2) t += s_x[w2][0][threadIdx.x];
       part[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = t;
     }
   } else {
+    // warps' Gram fragments summed in warp order through one R x R buffer
+    double t[PER];
 #pragma unroll
-    for (int mt2 = 0; mt2 < 2; ++mt2)
+    for (int q = 0; q < PER; ++q) t[q] = 0.0;
+    for (int w2 = 0; w2 < NW; ++w2) {
+      __syncthreads();
+      if (warp == w2) {
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+        for (int mt2 = 0; mt2 < NT; ++mt2)
 #pragma unroll
-        for (int q = 0; q < 2; ++q) s_red[warp][(8 * mt2 + gid) * R + 8 * nt + 2 * tig + q] = g[mt2][nt][q];
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < R * R; idx += kTcThreads) {
-      double t = 0.0;
-      for (int w2 = 0; w2 < NW; ++w2) t += s_red[w2][idx];
-      part[static_cast<long long>(blockIdx.x) * R * R + idx] = t;
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) s_red[(8 * mt2 + gid) * R + 8 * nt + 2 * tig + q] = g[mt2][nt][q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < PER; ++q) t[q] += s_red[threadIdx.x + q * kTcThreads];
     }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) part[static_cast<long long>(blockIdx.x) * R * R + threadIdx.x + q * kTcThreads] = t[q];
   }
 }
 
 // W = V^-1 = L^-T L^-1 from the Cholesky factor: one warp, lane j solves
 // column j of L^-1 (forward substitution), then W = Z^T Z.
-__global__ void inverse16_kernel(const double* __restrict__ lmat, double* __restrict__ w,
-                                 const int* __restrict__ status) {
-  constexpr int R = 16;
+template <int R>
+__global__ void inverse_kernel(const double* __restrict__ lmat, double* __restrict__ w,
+                               const int* __restrict__ status) {
   __shared__ double s_z[R][R + 1];  // L^-1, row-major
   if (*status == 2) return;
   const int j = threadIdx.x;
@@ -622,18 +638,17 @@ __global__ void inverse16_kernel(const double* __restrict__ lmat, double* __rest
   }
 }
 
-template <typename MT>
-int update16_tc_impl(const double* v, const MT* m, long long rows, double* x64, float* x32, double* lambda,
-                     double* gram, int* d_status, double* ws, cudaStream_t s) {
-  constexpr int R = 16;
+template <int R, typename MT>
+int update_tc_impl(const double* v, const MT* m, long long rows, double* x64, float* x32, double* lambda,
+                   double* gram, int* d_status, double* ws, cudaStream_t s) {
   double* part = ws;
   double* lmat = ws + static_cast<size_t>(kUpdBlocks) * R * R;
   double* winv = lmat + R * R;
   cholesky_kernel<<<1, 32, 0, s>>>(v, R, lmat, d_status);
-  inverse16_kernel<<<1, 32, 0, s>>>(lmat, winv, d_status);
-  update16_tc<MT, false><<<kUpdBlocks, kTcThreads, 0, s>>>(winv, m, rows, nullptr, x64, x32, d_status, part);
+  inverse_kernel<R><<<1, 32, 0, s>>>(lmat, winv, d_status);
+  update_tc<R, MT, false><<<kUpdBlocks, kTcThreads, 0, s>>>(winv, m, rows, nullptr, x64, x32, d_status, part);
   sum_partials_warp<<<(R + 7) / 8, 256, 0, s>>>(part, kUpdBlocks, R, lambda, 1, d_status);
-  update16_tc<MT, true><<<kUpdBlocks, kTcThreads, 0, s>>>(winv, m, rows, lambda, x64, x32, d_status, part);
+  update_tc<R, MT, true><<<kUpdBlocks, kTcThreads, 0, s>>>(winv, m, rows, lambda, x64, x32, d_status, part);
   sum_partials_warp<<<(R * R + 7) / 8, 256, 0, s>>>(part, kUpdBlocks, R * R, gram, 0, d_status);
   ALTO_LAUNCH_CHECK("alto_cpd_update(tc)");
   return ALTO_OK;
@@ -724,10 +739,15 @@ int alto_cpd_update(const double* v, const void* mttkrp, int32_t m_dtype, int64_
   auto* w = static_cast<double*>(ws);
   const bool scalar = (flags & 1) != 0;  // ALTO_CPD_SCALAR: substitution kernels instead of DMMA
   if (rank == 16 && !scalar)
-    return m_dtype == ALTO_F32 ? update16_tc_impl(v, static_cast<const float*>(mttkrp), rows, x64, x32, lambda, gram,
-                                                  d_status, w, s)
-                               : update16_tc_impl(v, static_cast<const double*>(mttkrp), rows, x64, x32, lambda,
-                                                  gram, d_status, w, s);
+    return m_dtype == ALTO_F32 ? update_tc_impl<16>(v, static_cast<const float*>(mttkrp), rows, x64, x32, lambda,
+                                                    gram, d_status, w, s)
+                               : update_tc_impl<16>(v, static_cast<const double*>(mttkrp), rows, x64, x32, lambda,
+                                                    gram, d_status, w, s);
+  if (rank == 32 && !scalar)
+    return m_dtype == ALTO_F32 ? update_tc_impl<32>(v, static_cast<const float*>(mttkrp), rows, x64, x32, lambda,
+                                                    gram, d_status, w, s)
+                               : update_tc_impl<32>(v, static_cast<const double*>(mttkrp), rows, x64, x32, lambda,
+                                                    gram, d_status, w, s);
   if (rank == 16)
     return m_dtype == ALTO_F32 ? update_impl<16>(v, static_cast<const float*>(mttkrp), rows, x64, x32, lambda, gram,
                                                  d_status, w, s)

@@ -1,5 +1,3 @@
 cd $GRAFT_REPO_ROOT; export PYTHONPATH=$GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests/test_gpu_cpd.py tests/test_gpu_dist.py -x -q 2>&1 | tail -3
-timeout 900 python tools/prof_cpals.py 5 2>&1 | tail -1
-timeout 600 python tools/prof_cpals.py 2 2>&1 | tail -1
-timeout 600 python tools/prof_cpals.py 4 2>&1 | tail -1
+timeout 600 python tools/prof_cpals.py 3 2>&1 | tail -1
