@@ -280,7 +280,8 @@ int alto_coalesce(const int64_t* coords, const double* values, int64_t m, int32_
 #define ALTO_STREAM_CTA_TILES 4  /* CTA-wide 1024-element tiles (cp.async staged)
                                     instead of warp-autonomous 128-element tiles */
 #define ALTO_STREAM_GENERIC 128  /* bypass the specialised (order 3-5, rank 16/32) kernels */
-#define ALTO_STREAM_TUNE_MINB2 256  /* tuning: 2 CTAs/SM launch bounds (default 3) */
+#define ALTO_STREAM_TUNE_MINB2 256  /* tuning: planned kernel: 2 CTAs/SM launch bounds (default 3);
+                                       mode-stream kernel (cfg2 shape): shuffle raw keys */
 #define ALTO_STREAM_TUNE_U4 512     /* tuning: planned kernel: 4 elements in flight per group (default 2);
                                        mode-stream kernel (cfg2 shape): record exchange through shared
                                        memory instead of shuffles */

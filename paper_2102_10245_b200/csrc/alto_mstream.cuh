@@ -130,7 +130,7 @@ struct MStream {
 };
 
 template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, bool COOP = false,
-          bool XCH_SHFL = false>
+          bool XCH_SHFL = false, bool XKEY = false>
 __global__ void __launch_bounds__(kTileThreads, MINB)
 mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStream S,
                const __grid_constant__ StreamParams P) {
@@ -301,7 +301,26 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
           V4<F> g[U][NIN];
           unsigned tg[U];
           V vu[U];
-          if constexpr (XCH_SHFL) {
+          if constexpr (XCH_SHFL && XKEY) {
+            // shuffle the raw key (2W words) and value; every lane decodes the
+            // fields itself (fewer shuffles than offsets + target + value
+            // when 2W < N, but measured slower on cfg2; A/B variant)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              Key<W> ku;
+#pragma unroll
+              for (int q = 0; q < W; ++q) {
+                const unsigned lo = __shfl_sync(0xffffffffu, static_cast<unsigned>(kk.w[q]), gbase + u);
+                const unsigned hi = __shfl_sync(0xffffffffu, static_cast<unsigned>(kk.w[q] >> 32), gbase + u);
+                ku.w[q] = (static_cast<uint64_t>(hi) << 32) | lo;
+              }
+              vu[u] = __shfl_sync(0xffffffffu, vv, gbase + u);
+              tg[u] = j0 + u < len ? target(ku) : 0xffffffffu;
+#pragma unroll
+              for (int k = 0; k < NIN; ++k)
+                if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], ms_field<W>(ku, fin[k]) * ROWB);
+            }
+          } else if constexpr (XCH_SHFL) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               tg[u] = __shfl_sync(0xffffffffu, mtg, gbase + u);
@@ -374,9 +393,9 @@ constexpr int ms_u() {
 }
 
 template <int W, typename V, typename O, int N, int R, bool COOP = true, int MINB = 3,
-          int U = ms_u<N, R, V, (COOP ? 32 : 16), COOP>(), bool XCH_SHFL = true>
+          int U = ms_u<N, R, V, (COOP ? 32 : 16), COOP>(), bool XCH_SHFL = true, bool XKEY = false>
 int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, cudaStream_t s) {
-  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, COOP, XCH_SHFL>;
+  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, COOP, XCH_SHFL, XKEY>;
   static int cached_bps = 0;
   if (!cached_bps) {
     int b = 1;
@@ -413,6 +432,9 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
       // shared-memory record exchange: 0.66-0.68 ms (fewer wavefronts, but
       // the two __syncwarp per block cost more than the shuffles)
       if (f == ALTO_STREAM_TUNE_U4) return launch_mstream<W, V, O, 3, 16, true, 3, 4, false>(d, S, P, s);
+      // shuffling the raw key + value (3 shuffles, every lane decodes) instead
+      // of offsets + target + value (4): 0.69-0.73 ms (decode costs more)
+      if (f == ALTO_STREAM_TUNE_MINB2) return launch_mstream<W, V, O, 3, 16, true, 3, 4, true, true>(d, S, P, s);
     }
   }
   if (P.rank == 16) {
