@@ -369,7 +369,7 @@ def run_b200(args):
     if ws > 1:
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
     e2e_ms = float(t_e.item())
-    h2d = N * sum(d * R * fb for d in dims)
+    h2d = sum(sum(d * R * fb for m, d in enumerate(dims) if m != n) for n in range(N))  # output factor not sent
     d2h = sum(d * R * 8 for d in dims)
 
     # CP-ALS iteration time (device loop, streaming backend), single GPU only

@@ -68,12 +68,21 @@ def _check_factors(dims: Sequence[int], factors, mode: int) -> int:
     return int(rank)
 
 
-def factors_to_device(factors, dtype=None) -> list:
-    """Factors as contiguous device tensors (float64 unless dtype/torch input says otherwise)."""
+def factors_to_device(factors, dtype=None, skip: int | None = None) -> list:
+    """Factors as contiguous device tensors (float64 unless dtype/torch input
+    says otherwise).  `skip`: a host factor the MTTKRP of that mode never
+    reads (the output mode's) is not copied; a 1-row placeholder of the same
+    dtype and rank stands in for it."""
     torch = _torch()
     dev = _lib.cuda_device()
     out = []
-    for f in factors:
+    for n, f in enumerate(factors):
+        if n == skip and not (isinstance(f, torch.Tensor) and f.is_cuda):
+            a = f if isinstance(f, torch.Tensor) else np.asarray(f)
+            is32 = (a.dtype == torch.float32) if isinstance(a, torch.Tensor) else (a.dtype == np.float32)
+            dt = dtype or (torch.float32 if is32 else torch.float64)
+            out.append(torch.zeros((1, int(a.shape[1])), dtype=dt, device=dev))
+            continue
         if isinstance(f, torch.Tensor):
             dt = dtype or (torch.float32 if f.dtype == torch.float32 else torch.float64)
             out.append(f.to(device=dev, dtype=dt).contiguous())
@@ -564,7 +573,7 @@ def mttkrp_oracle(tensor: CooTensor, factors, mode: int):
     rank = _check_factors(tensor.dims, factors, mode)
     dev = _lib.cuda_device()
     out = torch.empty((tensor.dims[mode], rank), dtype=torch.float64, device=dev)
-    fdev = factors_to_device(factors, torch.float64)
+    fdev = factors_to_device(factors, torch.float64, skip=mode)
     coords = torch.from_numpy(tensor.coords).to(dev)
     vals = torch.from_numpy(tensor.values).to(dev)
     arr = (ctypes.c_void_p * len(fdev))(*[f.data_ptr() for f in fdev])
@@ -577,7 +586,7 @@ def mttkrp_oracle(tensor: CooTensor, factors, mode: int):
 def mttkrp_seq(tensor: AltoTensor, factors, mode: int):
     """Sequential-order MTTKRP (mttkrp.py:108-117): exact-order engine, one partition."""
     _check_factors(tensor.layout.dims, factors, mode)
-    fdev = factors_to_device(factors)
+    fdev = factors_to_device(factors, skip=mode)
     return _finish(mttkrp_deterministic(tensor, fdev, mode), any(_is_torch(f) for f in factors))
 
 
@@ -602,7 +611,7 @@ def mttkrp_par(tensor: AltoTensor, parts: PartitionSet, plan: ConflictPlan, fact
         raise ValueError(f"plan is for mode {plan.mode}, kernel asked for {mode}")
     if not np.array_equal(plan.offsets, parts.offsets):
         raise ValueError("plan and partition set do not match")
-    fdev = factors_to_device(factors)
+    fdev = factors_to_device(factors, skip=mode)  # the output mode's factor is never read
     like = any(_is_torch(f) for f in factors)
     if plan.strategy is Strategy.BUFFERED:
         return _finish(mttkrp_deterministic(tensor, fdev, mode, np.asarray(parts.offsets)), like)

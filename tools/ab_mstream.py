@@ -68,7 +68,7 @@ def main():
             for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] == "mstream"]:
                 del alto._cache[k]
         mk.MS_TILE = tiles[0]
-        for fl, nm in ((256, "offset-shuffles"),):
+        for fl, nm in ((768, "minb4-u3"), (1280, "minb4-u2")):
             mk.STREAM_FLAGS = fl
             o = mttkrp_stream(alto, f, mode, out_dtype=fd)
             tm = timed(lambda: mttkrp_stream(alto, f, mode, out=o, out_dtype=fd), flush=flush)

@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT; export PYTHONPATH=$GRAFT_REPO_ROOT
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -8
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+timeout 900 python bench.py --steps 10 --skip-cpu --skip-cpals 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e'])"
