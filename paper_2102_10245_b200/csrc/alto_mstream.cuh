@@ -429,7 +429,9 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
       // 0.67-0.69, broadcast 0.70-0.72, cooperative at 2 CTAs/SM 0.75-0.79,
       // broadcast U=4 at 2 CTAs/SM 0.73-0.77
       if (f == ALTO_STREAM_MS_COOP) return launch_mstream<W, V, O, 3, 16, false>(d, S, P, s);
-      // (4 CTAs/SM at 64 registers with U=3 / U=2: 0.64-0.66 / 0.66-0.68 ms, dropped)
+      // (4 CTAs/SM at 64 registers with U=3 / U=2: 0.64-0.66 / 0.66-0.68 ms; a
+      // two-stage software pipeline of U=2 / U=3 blocks: 0.65-0.68 / 0.86-0.88
+      // ms — both dropped)
       // shared-memory record exchange: 0.66-0.68 ms (fewer wavefronts, but
       // the two __syncwarp per block cost more than the shuffles)
       if (f == ALTO_STREAM_TUNE_U4) return launch_mstream<W, V, O, 3, 16, true, 3, 4, false>(d, S, P, s);

@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT; export PYTHONPATH=$GRAFT_REPO_ROOT
-timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 900 python bench.py --steps 10 --skip-cpu --skip-cpals 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e'])"
+timeout 600 python tools/ab_mstream.py 2 0 1024 2>&1 | tail -3
+timeout 900 python tools/ab_mstream.py 5 0 1024 2>&1 | tail -3
