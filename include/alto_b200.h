@@ -250,9 +250,11 @@ int alto_subtile_order(const alto_layout* lay, const uint64_t* packed, int64_t m
  * hold ceil(m/tile)*tile elements (the tail is zero padding).  value_dtype
  * ALTO_F32 or ALTO_F64; tile a multiple of 256 with m / tile < 2^31. */
 size_t alto_mode_stream_workspace_bytes(int64_t m);
+#define ALTO_MS_ROW_MAJOR 1 /* flags: sort the whole stream by the mode's coordinate (stable: ALTO order
+                               within a row), not tile by tile */
 int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,
-                     int64_t m, int32_t mode, int32_t tile, const int32_t* hot_slot, uint64_t* skeys,
-                     void* svals, void* ws, size_t ws_bytes, void* stream);
+                     int64_t m, int32_t mode, int32_t tile, int32_t flags, const int32_t* hot_slot,
+                     uint64_t* skeys, void* svals, void* ws, size_t ws_bytes, void* stream);
 
 /* Hot-row copy plan of the mode-stream kernel: hot row s (hot_rows[s],
  * from alto_hot_rows) gets copies = 2^lg replicated partial rows, lg the

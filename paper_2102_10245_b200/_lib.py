@@ -102,7 +102,7 @@ SIGNATURES = [
     ("alto_hot_copies", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p,
                                   c_void_p]),
     ("alto_mode_stream", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32,
-                                   c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_topk_rows_workspace_bytes", c_size_t, [c_int64]),
     ("alto_topk_rows", c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_hot_rows", c_int32, [c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,

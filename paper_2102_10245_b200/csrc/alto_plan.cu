@@ -102,12 +102,12 @@ __global__ void subtile_order_kernel(const __grid_constant__ DevLayout L, const 
 // the per-tile stable sort by output row.
 template <int W>
 __global__ void mstream_keys_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ packed,
-                                    long long m, int mode, int tile, uint64_t* __restrict__ ckey,
+                                    long long m, int mode, int tile, int row_major, uint64_t* __restrict__ ckey,
                                     unsigned* __restrict__ idx) {
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m; i += stride) {
     const unsigned row = packed_field32<W>(load_key<W>(packed, i), L.pack_off[mode], L.bits[mode]);
-    ckey[i] = (static_cast<uint64_t>(i / tile) << L.bits[mode]) | row;
+    ckey[i] = row_major ? row : ((static_cast<uint64_t>(i / tile) << L.bits[mode]) | row);
     idx[i] = static_cast<unsigned>(i);
   }
 }
@@ -187,8 +187,8 @@ size_t alto_mode_stream_workspace_bytes(int64_t m) {
 }
 
 int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,
-                     int64_t m, int32_t mode, int32_t tile, const int32_t* hot_slot, uint64_t* skeys, void* svals,
-                     void* ws, size_t ws_bytes, void* stream) {
+                     int64_t m, int32_t mode, int32_t tile, int32_t flags, const int32_t* hot_slot, uint64_t* skeys,
+                     void* svals, void* ws, size_t ws_bytes, void* stream) {
   ALTO_REQUIRE(lay && lay->order >= 1 && lay->order <= ALTO_MAX_ORDER, "bad layout");
   ALTO_REQUIRE(mode >= 0 && mode < lay->order, "mode out of range");
   ALTO_REQUIRE(lay->bits[mode] <= 31, "mode stream needs mode extents below 2^31");
@@ -202,8 +202,9 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
     return ALTO_EUNSUPPORTED;
   }
   const long long ntiles = (m + tile - 1) / tile;
+  const int row_major = (flags & ALTO_MS_ROW_MAJOR) ? 1 : 0;
   int tbits = 0;
-  while ((1ll << tbits) < ntiles) ++tbits;
+  while (!row_major && (1ll << tbits) < ntiles) ++tbits;
   ALTO_REQUIRE(tbits + lay->bits[mode] <= 64, "too many tiles for the sort key");
   cudaStream_t s = as_stream(stream);
   const size_t vb = value_dtype == ALTO_F32 ? 4 : 8;
@@ -222,9 +223,9 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
   void* sws = static_cast<char*>(ws) + a + b;
   const int grid = grid_for(m, 256, kSMs * 8);
   if (d.n_words == 1)
-    mstream_keys_kernel<1><<<grid, 256, 0, s>>>(d, packed, m, mode, tile, ckey, idx);
+    mstream_keys_kernel<1><<<grid, 256, 0, s>>>(d, packed, m, mode, tile, row_major, ckey, idx);
   else
-    mstream_keys_kernel<2><<<grid, 256, 0, s>>>(d, packed, m, mode, tile, ckey, idx);
+    mstream_keys_kernel<2><<<grid, 256, 0, s>>>(d, packed, m, mode, tile, row_major, ckey, idx);
   ALTO_LAUNCH_CHECK("alto_mode_stream/keys");
   const int st = alto_sort_pairs(ckey, idx, m, 1, 4, tbits + lay->bits[mode], sws,
                                  ws_bytes - a - b, stream);

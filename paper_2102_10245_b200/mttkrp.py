@@ -295,6 +295,10 @@ def stream_plan(tensor: AltoTensor, mode: int, rank: int, fbytes: int):
 
 # Per-mode stream tile length (elements); 0 disables the mode-stream kernel.
 MS_TILE = int(__import__("os").environ.get("ALTO_MS_TILE", 1024))
+# Mode-stream order: 1 (default) = the whole stream sorted by the mode's
+# coordinate, ALTO order kept within a row (ALTO_MS_ROW_MAJOR); 0 = each tile
+# (a contiguous ALTO key range) sorted by it.
+MS_ORDER = int(__import__("os").environ.get("ALTO_MS_ORDER", 1))
 
 
 def ms_tile(tensor: AltoTensor) -> int:
@@ -314,7 +318,7 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
     torch = _torch()
     vals = tensor.vals if vals is None else vals
     T = ms_tile(tensor)
-    key = ("mstream", mode, vals.dtype, T)
+    key = ("mstream", mode, vals.dtype, T, MS_ORDER)
     hit = tensor._cache.get(key)
     if hit is None:
         lib = _lib.load()
@@ -329,7 +333,8 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
         wsb = int(lib.alto_mode_stream_workspace_bytes(m))
         ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
         rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals), m,
-                                  mode, T, hs[0].data_ptr() if hot else None, skeys.data_ptr(), svals.data_ptr(),
+                                  mode, T, MS_ORDER, hs[0].data_ptr() if hot else None, skeys.data_ptr(),
+                                  svals.data_ptr(),
                                   ws.data_ptr(), wsb, _lib.stream_ptr())
         del ws
         if rc == _lib.ALTO_EUNSUPPORTED:

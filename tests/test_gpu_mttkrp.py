@@ -262,18 +262,20 @@ class TestStreamKernel:
                 a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=variant).double().cpu().numpy()
                 assert rel_error(a, b) <= 1e-6, variant
 
+    @pytest.mark.parametrize("order", [0, 1])
     @pytest.mark.parametrize("cfg", [2, "wide", 4])
-    def test_mode_stream_layout(self, at, cfg):
-        """Per-mode stream (alto_mode_stream): each tile of T elements holds the
-        same elements as the ALTO stream's tile, stably sorted by the mode's
-        coordinate, stored as 8 interleaved slices; keys re-pack the
-        coordinates (input modes ascending, then the mode; no field straddles a
-        64-bit word) with the hot flag on the top bit."""
+    def test_mode_stream_layout(self, at, monkeypatch, cfg, order):
+        """Per-mode stream (alto_mode_stream): the ALTO stream stably sorted by
+        the mode's coordinate — as a whole (order 1, ALTO_MS_ROW_MAJOR) or tile
+        by tile (order 0) — cut into tiles of T stored as 8 interleaved slices;
+        keys re-pack the coordinates (input modes ascending, then the mode; no
+        field straddles a 64-bit word) with the hot flag on the top bit."""
         import importlib
 
         import torch
 
         mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+        monkeypatch.setattr(mk, "MS_ORDER", order)
         st = synth.make_tensor(self.WIDE if cfg == "wide" else cfg, nnz=60_001)
         dims = st.config.dims
         alto = at.build_alto(at.CooTensor(dims, st.coords, st.values.astype(np.float64)), dtype="float32")
@@ -290,9 +292,9 @@ class TestStreamKernel:
             assert tile == T
             sk = sk.cpu().numpy().view(np.uint64).reshape(-1, W)
             sv = sv.cpu().numpy()
-            order = [n for n in range(len(dims)) if n != mode] + [mode]
+            forder = [n for n in range(len(dims)) if n != mode] + [mode]
             cur, fields = 0, {}
-            for n in order:
+            for n in forder:
                 b = lay.bits[n]
                 if (cur % 64) + b > 64:
                     cur = (cur + 63) // 64 * 64
@@ -301,6 +303,7 @@ class TestStreamKernel:
             hs = mk.hot_slots(alto, mode)
             hot_rows = set() if hs is None else set(hs[1][:hs[2]].cpu().numpy().tolist())
             ch = T // 8
+            gperm = np.argsort(coords[:, mode], kind="stable")  # row-major order of the whole stream
             for t0 in list(range(0, alto.nnz, T))[::7] + [alto.nnz - 1 - (alto.nnz - 1) % T]:
                 cnt = min(T, alto.nnz - t0)
                 p = np.arange(cnt)
@@ -309,9 +312,12 @@ class TestStreamKernel:
                 dec = np.stack([(keys[:, fields[n][0]] >> np.uint64(fields[n][1])) & np.uint64((1 << fields[n][2]) - 1)
                                 for n in range(len(dims))], 1).astype(np.int64)
                 flag = (keys[:, W - 1] >> np.uint64(63)).astype(bool)
-                ref = np.argsort(coords[t0:t0 + cnt, mode], kind="stable")
-                assert np.array_equal(dec, coords[t0:t0 + cnt][ref])
-                assert np.array_equal(sv[idx], vals[t0:t0 + cnt][ref])
+                if order == 1:
+                    ref = gperm[t0:t0 + cnt]
+                else:
+                    ref = t0 + np.argsort(coords[t0:t0 + cnt, mode], kind="stable")
+                assert np.array_equal(dec, coords[ref])
+                assert np.array_equal(sv[idx], vals[ref])
                 assert np.array_equal(flag, np.array([r in hot_rows for r in dec[:, mode]]))
         rng = np.random.default_rng(4)
         fdev = mk.factors_to_device([rng.random((d, 16)).astype(np.float32) for d in dims])

@@ -68,14 +68,18 @@ def main():
             for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] == "mstream"]:
                 del alto._cache[k]
         mk.MS_TILE = tiles[0]
-        for fl, nm in ((768, "minb4-u3"), (1280, "minb4-u2")):
-            mk.STREAM_FLAGS = fl
+        for fl, nm in ((-1, "tile-order"),):
+            mk.MS_ORDER = 0 if fl == -1 else 1
+            for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] in ("mstream", "hotms")]:
+                del alto._cache[k]
+            mk.STREAM_FLAGS = max(fl, 0)
             o = mttkrp_stream(alto, f, mode, out_dtype=fd)
             tm = timed(lambda: mttkrp_stream(alto, f, mode, out=o, out_dtype=fd), flush=flush)
             o = mttkrp_stream(alto, f, mode, out_dtype=fd).double()
             line.append(f"{nm}: {tm:.3f} ms (rel {float((o - ref).norm() / ref.norm()):.1e})")
         mk.STREAM_FLAGS = 0
-        for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] == "mstream"]:
+        mk.MS_ORDER = 1
+        for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] in ("mstream", "hotms")]:
             del alto._cache[k]
         print("; ".join(line), flush=True)
 
