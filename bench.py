@@ -329,7 +329,7 @@ def run_b200(args):
     for n in range(N):
         launches_per_step += 1
         if not args.no_hot:
-            hp = (alto._cache.get(("hotms", n, R, odt, mk.ms_tile(alto))) if ms_used
+            hp = (alto._cache.get(("hotms", n, R, odt, mk.ms_tile(alto), mk.MS_ORDER)) if ms_used
                   else alto._cache.get(("hot", n, R, odt)))
             launches_per_step += 1 if hp else 0
     tot_t = sum(mode_ms) * 1e-3

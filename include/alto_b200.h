@@ -258,12 +258,14 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
 
 /* Hot-row copy plan of the mode-stream kernel: hot row s (hot_rows[s],
  * from alto_hot_rows) gets copies = 2^lg replicated partial rows, lg the
- * smallest with 2^lg * bound >= estimated merges (min(count, tiles) +
+ * smallest with 2^lg * bound >= estimated merges (count/(tile/8) + 2 for a
+ * row-major stream, flags & ALTO_MS_ROW_MAJOR; else min(count, tiles) +
  * count/(tile/8)), lg <= max_lg; copies are laid out slot by slot:
  * hot_base[s] = first copy (n_hot+1 entries), hot_code[row] = (hot_base << 5)
  * | lg.  hot_code must be pre-filled with -1 for the other rows. */
 int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_hot, int64_t m, int32_t tile,
-                    int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base, void* stream);
+                    int32_t flags, int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base,
+                    void* stream);
 
 /* COO coalesce on the device (coo.py:97-114): rows sorted lexicographically
  * with mode 0 as the primary key (stable), duplicates summed in float64 in

@@ -99,8 +99,8 @@ SIGNATURES = [
                                 c_void_p, c_size_t, c_void_p]),
     ("alto_cpd_update", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
-    ("alto_hot_copies", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p,
-                                  c_void_p]),
+    ("alto_hot_copies", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p,
+                                  c_void_p, c_void_p]),
     ("alto_mode_stream", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32,
                                    c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_topk_rows_workspace_bytes", c_size_t, [c_int64]),

@@ -455,8 +455,8 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
 
 // out[row(s)] += sum of the row's copies (float64, fixed order), copies re-zeroed.
 // One warp per hot row; lane (j, r): rank r of copies j, j + 32/R, ... with
-// 4 independent accumulators (copies k = j + (4q + a)·32/R go to accumulator
-// a), then a fixed-order combine across accumulators and lanes.
+// 8 independent accumulators (copy j + (8q + a)·32/R goes to accumulator a),
+// then a fixed-order combine across accumulators and lanes.
 template <typename O>
 __global__ void __launch_bounds__(256) hot_reduce_rows_kernel(O* __restrict__ buf, const int* __restrict__ hot_rows,
                                                               const int* __restrict__ hot_base, int n_hot, int R,
@@ -469,29 +469,31 @@ __global__ void __launch_bounds__(256) hot_reduce_rows_kernel(O* __restrict__ bu
   const int r = lane % R, j = lane / R;
   const bool active = R >= 32 ? (lane < R) : (j < per);
   const int b0 = hot_base[slot], b1 = hot_base[slot + 1];
-  S acc[4] = {S(0), S(0), S(0), S(0)};
+  constexpr int NA = 8;  // independent accumulators = loads in flight per lane
+  S acc[NA];
+#pragma unroll
+  for (int q = 0; q < NA; ++q) acc[q] = S(0);
   if (active) {
+    const long long st = static_cast<long long>(per) * R;
     int k = b0 + j;
-    for (; k + 3 * per < b1; k += 4 * per) {
+    for (; k + (NA - 1) * per < b1; k += NA * per) {
       O* p = buf + static_cast<long long>(k) * R + r;
-      const long long st = static_cast<long long>(per) * R;
-      const O v0 = p[0], v1 = p[st], v2 = p[2 * st], v3 = p[3 * st];
-      acc[0] += static_cast<S>(v0);
-      acc[1] += static_cast<S>(v1);
-      acc[2] += static_cast<S>(v2);
-      acc[3] += static_cast<S>(v3);
-      p[0] = O(0);
-      p[st] = O(0);
-      p[2 * st] = O(0);
-      p[3 * st] = O(0);
+      O v[NA];
+#pragma unroll
+      for (int q = 0; q < NA; ++q) v[q] = p[q * st];
+#pragma unroll
+      for (int q = 0; q < NA; ++q) {
+        acc[q] += static_cast<S>(v[q]);
+        p[q * st] = O(0);
+      }
     }
-    for (int a = 0; k < b1; k += per, ++a) {
+    for (int q = 0; k < b1; k += per, ++q) {
       O* p = buf + static_cast<long long>(k) * R + r;
-      acc[a] += static_cast<S>(*p);
+      acc[q] += static_cast<S>(*p);
       *p = O(0);
     }
   }
-  S t = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  S t = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   // lanes r, r+R, ... hold rank r: fold in a fixed order
   for (int o = 16; o >= R && o > 0; o >>= 1) {
     const S u = __shfl_down_sync(0xffffffffu, t, o);

@@ -53,15 +53,18 @@ __global__ void __launch_bounds__(256) hot_reduce_kernel(B* __restrict__ buf, co
 // / bound, clamped to [1, 2^max_lg]; estimated merges = min(count, ntiles) +
 // count / (tile/8) (one run per tile, plus one per slice the row spans).
 __global__ void hot_copies_kernel(const long long* __restrict__ row_ptr, const int* __restrict__ hot_rows, int n_hot,
-                                  long long ntiles, int tile, int bound, int max_lg, int* __restrict__ hot_code,
-                                  int* __restrict__ hot_base) {
+                                  long long ntiles, int tile, int row_major, int bound, int max_lg,
+                                  int* __restrict__ hot_code, int* __restrict__ hot_base) {
   __shared__ int s_part[1024];
   const int per = (n_hot + blockDim.x - 1) / blockDim.x;
   const int s0 = threadIdx.x * per, s1 = min(n_hot, s0 + per);
   auto lg_of = [&](int s) {
     const long long r = hot_rows[s];
     const long long c = row_ptr[r + 1] - row_ptr[r];
-    const long long est = min(c, ntiles) + c / max(1, tile / kMsSlices);
+    // merges of a row: row-major stream -> one per slice it spans (+ the two
+    // partial ends); tile order -> up to one per tile plus one per slice
+    const long long per_slice = c / max(1, tile / kMsSlices);
+    const long long est = row_major ? per_slice + 2 : min(c, ntiles) + per_slice;
     const long long want = (est + bound - 1) / bound;
     int lg = 0;
     while (lg < max_lg && (1ll << lg) < want) ++lg;
@@ -238,13 +241,15 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
 }
 
 int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_hot, int64_t m, int32_t tile,
-                    int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base, void* stream) {
+                    int32_t flags, int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base,
+                    void* stream) {
   ALTO_REQUIRE(n_hot >= 0 && tile >= 256 && bound >= 1 && max_lg >= 0 && max_lg <= 20, "bad hot copy plan arguments");
   ALTO_REQUIRE(static_cast<long long>(n_hot) << max_lg < (1ll << 26), "too many hot-row copies");
   if (n_hot == 0) return ALTO_OK;
   cudaStream_t s = as_stream(stream);
   hot_copies_kernel<<<1, 1024, 0, s>>>(reinterpret_cast<const long long*>(row_ptr), hot_rows, n_hot,
-                                       (m + tile - 1) / tile, tile, bound, max_lg, hot_code, hot_base);
+                                       (m + tile - 1) / tile, tile, (flags & ALTO_MS_ROW_MAJOR) ? 1 : 0, bound,
+                                       max_lg, hot_code, hot_base);
   ALTO_LAUNCH_CHECK("alto_hot_copies");
   return ALTO_OK;
 }

@@ -200,7 +200,7 @@ def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype):
     (hot_code (I_mode,) int32, hot rows, count, hot_base (count+1,) int32, zeroed copies) or None."""
     torch = _torch()
     T = ms_tile(tensor)
-    key = ("hotms", mode, rank, out_dtype, T)
+    key = ("hotms", mode, rank, out_dtype, T, MS_ORDER)
     if key in tensor._cache:
         return tensor._cache[key]
     hs = hot_slots(tensor, mode)
@@ -211,7 +211,7 @@ def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype):
         _perm, ptr = row_index(tensor, mode)
         code = torch.full((tensor.layout.dims[mode],), -1, dtype=torch.int32, device=dev)
         base = torch.empty(n + 1, dtype=torch.int32, device=dev)
-        _lib.check(_lib.load().alto_hot_copies(ptr.data_ptr(), rows.data_ptr(), n, tensor.nnz, T, HOT_BOUND,
+        _lib.check(_lib.load().alto_hot_copies(ptr.data_ptr(), rows.data_ptr(), n, tensor.nnz, T, MS_ORDER, HOT_BOUND,
                                                HOT_MAX_LG, code.data_ptr(), base.data_ptr(), _lib.stream_ptr()),
                    "alto_hot_copies")
         total = int(base[n].item())

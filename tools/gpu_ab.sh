@@ -1,5 +1,3 @@
 cd $GRAFT_REPO_ROOT; export PYTHONPATH=$GRAFT_REPO_ROOT
-timeout 1500 python -m pytest tests/test_gpu_mttkrp.py tests/test_gpu_cpd.py -q -x 2>&1 | tail -2
-timeout 600 python tools/ab_mstream.py 2 0 1024 2>&1 | tail -3
-timeout 900 python tools/ab_mstream.py 5 0 1024 2>&1 | tail -3
-timeout 900 python tools/ab_mstream.py 4 0 1024 2>&1 | tail -5
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+timeout 900 python bench.py --steps 20 --skip-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], [p['kernel_ms'] for p in d['roofline']['per_mode']], d['cpals_ms_per_iter'])"
