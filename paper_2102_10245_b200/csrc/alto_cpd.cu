@@ -614,28 +614,74 @@ __global__ void __launch_bounds__(kTcThreads) update_tc(const double* __restrict
   }
 }
 
-// W = V^-1 = L^-T L^-1 from the Cholesky factor: one warp, lane j solves
-// column j of L^-1 (forward substitution), then W = Z^T Z.
+// Cholesky of V with the ridge retry of cholesky_kernel (cpd.py:80-95) and
+// W = V^-1 = L^-T L^-1, by one warp (rank <= 32): column j of L is one
+// warp reduction for the pivot plus one lane per row below it; column j of
+// L^-1 is lane j's forward substitution; W entries are spread over lanes.
 template <int R>
-__global__ void inverse_kernel(const double* __restrict__ lmat, double* __restrict__ w,
-                               const int* __restrict__ status) {
-  __shared__ double s_z[R][R + 1];  // L^-1, row-major
+__global__ void chol_inv_kernel(const double* __restrict__ v, double* __restrict__ w, int* __restrict__ status) {
+  static_assert(R <= 32, "one lane per row");
+  __shared__ double a[R][R + 1];
+  __shared__ double z[R][R + 1];
+  const int lane = threadIdx.x;
   if (*status == 2) return;
-  const int j = threadIdx.x;
-  if (j < R) {
+  bool finite = true;
+  double tr = 0.0;
+  for (int i = 0; i < R; ++i) {
+    const double x = lane < R ? v[i * R + lane] : 0.0;
+    finite &= static_cast<bool>(isfinite(x));
+    if (lane == i) tr = x;
+  }
+  finite = __all_sync(0xffffffffu, finite);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);  // trace (all lanes)
+  auto factor = [&](double ridge) -> bool {
+    if (lane < R)
+      for (int i = 0; i < R; ++i) a[i][lane] = v[i * R + lane] + (i == lane ? ridge : 0.0);
+    __syncwarp();
+    for (int j = 0; j < R; ++j) {
+      double t = lane < j ? a[j][lane] * a[j][lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      const double d = a[j][j] - t;
+      if (!(d > 0.0) || !isfinite(d)) return false;  // warp-uniform
+      const double l = sqrt(d);
+      if (lane > j && lane < R) {
+        double sum = a[lane][j];
+        for (int k = 0; k < j; ++k) sum -= a[lane][k] * a[j][k];
+        a[lane][j] = sum / l;
+      }
+      __syncwarp();
+      if (lane == 0) a[j][j] = l;
+      __syncwarp();
+    }
+    return true;
+  };
+  int st = 0;
+  if (!(finite && factor(0.0))) {
+    const double ridge = 1e-12 * tr / R;
+    st = (finite && isfinite(ridge) && factor(ridge)) ? 1 : 2;
+  }
+  if (st == 2) {
+    if (lane == 0 && st > *status) *status = st;
+    return;
+  }
+  if (lane < R) {  // column `lane` of L^-1
+    const int j = lane;
     for (int i = 0; i < R; ++i) {
-      double v = i == j ? 1.0 : 0.0;
-      for (int k = j; k < i; ++k) v -= lmat[i * R + k] * s_z[k][j];
-      s_z[i][j] = i < j ? 0.0 : v / lmat[i * R + i];
+      double x = i == j ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) x -= a[i][k] * z[k][j];
+      z[i][j] = i < j ? 0.0 : x / a[i][i];
     }
   }
   __syncwarp();
-  for (int idx = threadIdx.x; idx < R * R; idx += 32) {
+  for (int idx = lane; idx < R * R; idx += 32) {
     const int r = idx / R, c = idx % R;
-    double v = 0.0;
-    for (int k = (r > c ? r : c); k < R; ++k) v += s_z[k][r] * s_z[k][c];
-    w[idx] = v;
+    double x = 0.0;
+    for (int k = (r > c ? r : c); k < R; ++k) x += z[k][r] * z[k][c];
+    w[idx] = x;
   }
+  if (lane == 0 && st > *status) *status = st;
 }
 
 template <int R, typename MT>
@@ -644,8 +690,8 @@ int update_tc_impl(const double* v, const MT* m, long long rows, double* x64, fl
   double* part = ws;
   double* lmat = ws + static_cast<size_t>(kUpdBlocks) * R * R;
   double* winv = lmat + R * R;
-  cholesky_kernel<<<1, 32, 0, s>>>(v, R, lmat, d_status);
-  inverse_kernel<R><<<1, 32, 0, s>>>(lmat, winv, d_status);
+  chol_inv_kernel<R><<<1, 32, 0, s>>>(v, winv, d_status);
+  (void)lmat;
   update_tc<R, MT, false><<<kUpdBlocks, kTcThreads, 0, s>>>(winv, m, rows, nullptr, x64, x32, d_status, part);
   sum_partials_warp<<<(R + 7) / 8, 256, 0, s>>>(part, kUpdBlocks, R, lambda, 1, d_status);
   update_tc<R, MT, true><<<kUpdBlocks, kTcThreads, 0, s>>>(winv, m, rows, lambda, x64, x32, d_status, part);
