@@ -68,15 +68,44 @@ def _check_factors(dims: Sequence[int], factors, mode: int) -> int:
     return int(rank)
 
 
+_COPY_STREAM = {}
+
+
+def _copy_stream(dev):
+    """Side stream for host->device factor copies (one per device)."""
+    torch = _torch()
+    st = _COPY_STREAM.get(dev)
+    if st is None:
+        st = torch.cuda.Stream(device=dev)
+        _COPY_STREAM[dev] = st
+    return st
+
+
 def factors_to_device(factors, dtype=None, skip: int | None = None) -> list:
     """Factors as contiguous device tensors (float64 unless dtype/torch input
     says otherwise).  `skip`: a host factor the MTTKRP of that mode never
     reads (the output mode's) is not copied; a 1-row placeholder of the same
-    dtype and rank stands in for it."""
+    dtype and rank stands in for it.  Pinned host torch tensors are copied
+    asynchronously on a side stream that the current stream then waits for,
+    so a caller's next upload overlaps the previous call's kernels (as with
+    any non_blocking copy, a pinned input must not be modified until the
+    stream is synchronized)."""
     torch = _torch()
     dev = _lib.cuda_device()
     out = []
+    cur = None
     for n, f in enumerate(factors):
+        if (isinstance(f, torch.Tensor) and not f.is_cuda and f.is_pinned() and n != skip
+                and (dtype is None or f.dtype == dtype) and f.is_contiguous()):
+            if cur is None:
+                cur = torch.cuda.current_stream(dev)
+                side = _copy_stream(dev)
+            with torch.cuda.stream(side):
+                d = torch.empty(f.shape, dtype=f.dtype, device=dev)  # side-stream memory pool
+                d.copy_(f, non_blocking=True)
+            d.record_stream(cur)  # not reused before the work queued on `cur` that reads it
+            out.append(d)
+            continue
         if n == skip and not (isinstance(f, torch.Tensor) and f.is_cuda):
             a = f if isinstance(f, torch.Tensor) else np.asarray(f)
             is32 = (a.dtype == torch.float32) if isinstance(a, torch.Tensor) else (a.dtype == np.float32)
@@ -90,6 +119,8 @@ def factors_to_device(factors, dtype=None, skip: int | None = None) -> list:
             a = np.asarray(f)
             dt = dtype or (torch.float32 if a.dtype == np.float32 else torch.float64)
             out.append(torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dt).contiguous())
+    if cur is not None:
+        cur.wait_stream(_copy_stream(dev))
     return out
 
 

@@ -415,3 +415,32 @@ class TestStreamKernel:
         a = mttkrp_stream(alto, f, 1)
         b = mttkrp_stream(two, f, 1)
         assert rel_error(b.cpu().numpy(), 2 * a.cpu().numpy()) <= 1e-6
+
+
+def test_pinned_inputs_async_upload(at):
+    """Pinned host torch factors are uploaded on a side stream that overlaps
+    the previous call's kernels; back-to-back calls (no host sync between)
+    give the results of NumPy inputs (to float32-atomic rounding: the Atomic
+    plan's merge order is not fixed)."""
+    import torch
+
+    st = synth.make_tensor(2, nnz=200_000)
+    dims = st.config.dims
+    alto = at.build_alto(at.CooTensor(dims, st.coords, st.values.astype(np.float64)), dtype="float32")
+    parts = at.partition(alto, 8)
+    rng = np.random.default_rng(9)
+    sets = [[rng.random((d, 16)).astype(np.float32) for d in dims] for _ in range(4)]
+    plans = [at.plan_conflicts(alto, parts, n, force_strategy=at.Strategy.ATOMIC) for n in range(3)]
+    flagged = [at.apply_boundary_flags(alto, p) if p.flag_bit is not None else alto for p in plans]
+    outs = []
+    for fs in sets:
+        pinned = [torch.from_numpy(f).pin_memory() for f in fs]
+        for n in range(3):
+            outs.append(at.mttkrp_par(flagged[n], parts, plans[n], pinned, n))
+    torch.cuda.synchronize()
+    k = 0
+    for fs in sets:
+        for n in range(3):
+            ref = at.mttkrp_par(flagged[n], parts, plans[n], fs, n)
+            assert rel_error(outs[k].cpu().numpy(), ref) <= 1e-6
+            k += 1
