@@ -24,6 +24,8 @@ from .mttkrp import (F32_ACCUMULATE, _check_factors, factors_to_device, mttkrp_d
                      mttkrp_seq, mttkrp_stream)
 
 BACKENDS = ("seq", "oracle", "auto", "buffered", "atomic")
+# Replay the per-mode updates of a sweep as one CUDA graph (after the first sweep)
+CPD_GRAPHS = __import__("os").environ.get("ALTO_CPD_GRAPHS", "1") == "1"
 # alto_cpd_update flags (ALTO_CPD_SCALAR = 1: scalar substitution instead of the rank-16 DMMA path)
 CPD_UPDATE_FLAGS = int(__import__("os").environ.get("ALTO_CPD_FLAGS", "0"))
 
@@ -281,6 +283,8 @@ class DeviceCpAls:
         self.norm_sq = sumsq_device(tensor.vals, self.ws)
         self.v = torch.empty((rank, rank), dtype=torch.float64, device=dev)
         self.m_last = None
+        self._graph = None
+        self._graph_m = None
 
     def gather_factors(self):
         return self.f32 if self.use32 else self.f64
@@ -325,10 +329,39 @@ class DeviceCpAls:
             m = m64
         return _device_fit(self.norm_sq, self.f64, self.grams, self.lam, m, mode, self.ws)
 
-    def sweep(self) -> float:
-        order = self.tensor.layout.order
-        for mode in range(order):
+    def _updates(self):
+        m = None
+        for mode in range(self.tensor.layout.order):
             m = self.update(mode)
+        return m
+
+    def sweep(self) -> float:
+        """One ALS sweep (all modes) and its fit.  After the first (eager)
+        sweep the per-mode updates are captured once in a CUDA graph and
+        replayed: every kernel and workspace is static by then (plans,
+        hot-row copies and launch configurations are cached), and a replay
+        removes the host launch gaps between the ~30 small launches of a
+        sweep.  Set CPD_GRAPHS = False (ALTO_CPD_GRAPHS=0) to run eagerly."""
+        torch = _torch()
+        order = self.tensor.layout.order
+        if not CPD_GRAPHS or self._graph is False:
+            m = self._updates()
+        elif self._graph is None:
+            m = self._updates()  # eager warm-up: builds every cache the capture needs
+            torch.cuda.synchronize()
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._graph_m = self._updates()
+                self._graph = g
+                self.m_last = m  # the capture recorded, but did not run, the updates
+            except Exception:  # capture unsupported here: stay eager (same kernels)
+                self._graph = False
+                torch.cuda.synchronize()
+        else:
+            self._graph.replay()
+            m = self._graph_m
+            self.m_last = m
         self.check_status()
         return self.fit(m, order - 1)
 
