@@ -322,7 +322,8 @@ def run_b200(args):
     # our kernels per step: the streaming MTTKRP of each mode + its hot-row
     # reduction when the mode has hot rows (the output zeroing is a memset)
     mk = __import__("importlib").import_module("paper_2102_10245_b200.mttkrp")
-    ms_used = all(alto._cache.get(("mstream", n, alto.vals.dtype, mk.ms_tile(alto), mk.MS_ORDER)) for n in range(N))
+    ms_used = all(alto._cache.get(("mstream", n, alto.vals.dtype, mk.ms_tile(alto), mk.MS_ORDER, mk.MS_RR))
+                  for n in range(N))
     kernel_name = ("alto::mstream_kernel (alto_mstream.cuh)" if ms_used
                    else "alto::planned_kernel (alto_fast.cuh)")
     launches_per_step = 0

@@ -193,6 +193,7 @@ typedef struct alto_mttkrp_args {
    * the per-slot first copy (n_hot+1), and hot_buf hot_base[n_hot] * rank
    * elements of out_dtype (zero on entry, left zero). */
   const int32_t* hot_base;
+  int32_t mrr;                   /* mode stream built with ALTO_MS_ROUND_ROBIN */
 } alto_mttkrp_args;
 
 /* Deterministic MTTKRP support (ALTO_I64 output).  alto_sumabs / alto_absmax:
@@ -252,6 +253,8 @@ int alto_subtile_order(const alto_layout* lay, const uint64_t* packed, int64_t m
 size_t alto_mode_stream_workspace_bytes(int64_t m);
 #define ALTO_MS_ROW_MAJOR 1 /* flags: sort the whole stream by the mode's coordinate (stable: ALTO order
                                within a row), not tile by tile */
+#define ALTO_MS_ROUND_ROBIN 4 /* flags: lane group s of a tile takes sorted positions s, s+8, ... (stream
+                                 stored in sorted order) instead of a contiguous slice */
 int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,
                      int64_t m, int32_t mode, int32_t tile, int32_t flags, const int32_t* hot_slot,
                      uint64_t* skeys, void* svals, void* ws, size_t ws_bytes, void* stream);

@@ -66,6 +66,7 @@ class CMttkrpArgs(Structure):
         ("mvals", c_void_p),
         ("mtile", c_int32),
         ("hot_base", c_void_p),
+        ("mrr", c_int32),
     ]
 
 

@@ -127,6 +127,7 @@ struct MStream {
   const void* vals;      // (ntiles*T,) values
   int tile;              // T (multiple of 256)
   MsFields f;
+  int rr;                // round-robin slices: group s takes sorted positions s, s+8, ...
 };
 
 template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, bool COOP = false,
@@ -185,7 +186,7 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
 #pragma unroll 1
     for (int pass = 0; pass < PASSES; ++pass) {
       const int s = pass * GPW + grp;
-      const int len = max(0, min(CH, cnt - s * CH));
+      const int len = S.rr ? max(0, (cnt - s + kMsSlices - 1) / kMsSlices) : max(0, min(CH, cnt - s * CH));
       const uint64_t* kp = S.keys + (tb + s) * W;
       const V* vp = vals + tb + s;
       A acc[4] = {A(0), A(0), A(0), A(0)};
@@ -419,7 +420,7 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
   if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
   for (int n = 0; n < d.order; ++n)
     if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
-  const MStream S{P.mkeys, P.mvals, P.mtile, ms_fields(d, P.mode)};
+  const MStream S{P.mkeys, P.mvals, P.mtile, ms_fields(d, P.mode), P.mrr};
   if (!S.f.ok) return ALTO_EUNSUPPORTED;
   if constexpr (W == 1 && sizeof(V) == 4 && sizeof(O) == 4) {
     // tuning variants for the cfg2 shape (A/B only)

@@ -116,15 +116,18 @@ template <int W, typename V>
 __global__ void mstream_scatter_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MsFields F,
                                        const uint64_t* __restrict__ packed, const V* __restrict__ vals,
                                        const unsigned* __restrict__ idx, long long m, int mode, int tile,
-                                       const int* __restrict__ hot_slot, uint64_t* __restrict__ skeys,
-                                       V* __restrict__ svals) {
+                                       int round_robin, const int* __restrict__ hot_slot,
+                                       uint64_t* __restrict__ skeys, V* __restrict__ svals) {
   const int ch = tile / kMsSlices;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < m; q += stride) {
     const long long src = idx[q];
     const long long t = q / tile;
     const int p = static_cast<int>(q - t * tile);
-    const long long dst = t * tile + static_cast<long long>(p % ch) * kMsSlices + p / ch;
+    // slices: lane group s takes sorted positions [s*ch, (s+1)*ch) of the tile,
+    // stored interleaved; round robin: group s takes positions s, s+8, ...
+    // (consecutive elements in one instruction), stored in sorted order
+    const long long dst = round_robin ? q : t * tile + static_cast<long long>(p % ch) * kMsSlices + p / ch;
     const Key<W> k = load_key<W>(packed, src);
     Key<W> o{};
     for (int n = 0; n < L.order; ++n) {
@@ -233,7 +236,8 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
   const int* hs = reinterpret_cast<const int*>(hot_slot);
 #define ALTO_MS_SCATTER(WW, VT)                                                                              \
   mstream_scatter_kernel<WW, VT><<<grid, 256, 0, s>>>(d, F, packed, static_cast<const VT*>(values), idx, m, mode, \
-                                                      tile, hs, skeys, static_cast<VT*>(svals))
+                                                      tile, (flags & ALTO_MS_ROUND_ROBIN) ? 1 : 0, hs, skeys,    \
+                                                      static_cast<VT*>(svals))
   if (d.n_words == 1) {
     if (vb == 4) ALTO_MS_SCATTER(1, float); else ALTO_MS_SCATTER(1, double);
   } else {

@@ -167,6 +167,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.mkeys = a->mkeys;
   P.mvals = a->mvals;
   P.mtile = a->mtile;
+  P.mrr = a->mrr;
   ALTO_REQUIRE(!a->mkeys || (a->mvals && a->mtile >= 256 && a->mtile % 256 == 0),
                "mode stream needs values and a tile that is a multiple of 256");
   ALTO_REQUIRE(!a->mkeys || a->n_hot <= 0 || a->hot_base, "mode-stream hot plan needs hot_base");

@@ -65,6 +65,7 @@ struct StreamParams {
   const uint64_t* mkeys;      // per-mode stream (optional, alto_mode_stream): keys
   const void* mvals;          //   values
   int mtile;                  //   tile length T
+  int mrr;                    //   round-robin slices (ALTO_MS_ROUND_ROBIN)
   const double* fixed_scale;  // deterministic mode: device scalar, int64 output = round(x * scale)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
 };
 

@@ -330,6 +330,10 @@ MS_TILE = int(__import__("os").environ.get("ALTO_MS_TILE", 1024))
 # coordinate, ALTO order kept within a row (ALTO_MS_ROW_MAJOR); 0 = each tile
 # (a contiguous ALTO key range) sorted by it.
 MS_ORDER = int(__import__("os").environ.get("ALTO_MS_ORDER", 1))
+# Lane groups take round-robin positions of a tile (1, default: the 8 elements
+# of one warp instruction are consecutive, so their ALTO-ordered input rows
+# share lines more often) or contiguous slices (0).
+MS_RR = int(__import__("os").environ.get("ALTO_MS_RR", 1))
 
 
 def ms_tile(tensor: AltoTensor) -> int:
@@ -349,7 +353,7 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
     torch = _torch()
     vals = tensor.vals if vals is None else vals
     T = ms_tile(tensor)
-    key = ("mstream", mode, vals.dtype, T, MS_ORDER)
+    key = ("mstream", mode, vals.dtype, T, MS_ORDER, MS_RR)
     hit = tensor._cache.get(key)
     if hit is None:
         lib = _lib.load()
@@ -364,7 +368,8 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
         wsb = int(lib.alto_mode_stream_workspace_bytes(m))
         ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
         rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals), m,
-                                  mode, T, MS_ORDER, hs[0].data_ptr() if hot else None, skeys.data_ptr(),
+                                  mode, T, MS_ORDER | (4 if MS_RR else 0), hs[0].data_ptr() if hot else None,
+                                  skeys.data_ptr(),
                                   svals.data_ptr(),
                                   ws.data_ptr(), wsb, _lib.stream_ptr())
         del ws
@@ -372,9 +377,14 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
             hit = False  # field layout does not fit the key width: planned kernel instead
         else:
             _lib.check(rc, "alto_mode_stream")
-            hit = (skeys, svals, T)
+            hit = (skeys, svals, T, MS_RR)
         tensor._cache[key] = hit
     return hit or None
+
+
+def _set_stream(a, ms) -> None:
+    sk, sv, st, rr = ms
+    a.mkeys, a.mvals, a.mtile, a.mrr = sk.data_ptr(), sv.data_ptr(), st, 1 if rr else 0
 
 
 def _use_mode_stream(tensor: AltoTensor, rank: int, fbytes: int = 4) -> bool:
@@ -439,8 +449,7 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
     ms = (mode_stream(tensor, mode) if planned is True and PLAN_VARIANT == "pos"
           and _use_mode_stream(tensor, rank, fdev[0].element_size()) else None)
     if ms is not None:
-        sk, sv, st = ms
-        a.mkeys, a.mvals, a.mtile = sk.data_ptr(), sv.data_ptr(), st
+        _set_stream(a, ms)
     elif planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
             and max(tensor.layout.bits) <= 31:
         a.packed = packed_keys(tensor).data_ptr()
@@ -553,8 +562,7 @@ def mttkrp_det(tensor: AltoTensor, fdev: list, mode: int, out=None):
     a.fixed_scale = scale.data_ptr()
     ms = mode_stream(tensor, mode, vals) if _use_mode_stream(tensor, rank, fdev[0].element_size()) else None
     if ms is not None:
-        sk, sv, st = ms
-        a.mkeys, a.mvals, a.mtile = sk.data_ptr(), sv.data_ptr(), st
+        _set_stream(a, ms)
     else:
         a.packed = packed_keys(tensor).data_ptr()
         a.pos = subtile_order(tensor, mode).data_ptr()

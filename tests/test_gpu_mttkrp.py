@@ -262,9 +262,10 @@ class TestStreamKernel:
                 a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=variant).double().cpu().numpy()
                 assert rel_error(a, b) <= 1e-6, variant
 
+    @pytest.mark.parametrize("rrobin", [0, 1])
     @pytest.mark.parametrize("order", [0, 1])
     @pytest.mark.parametrize("cfg", [2, "wide", 4])
-    def test_mode_stream_layout(self, at, monkeypatch, cfg, order):
+    def test_mode_stream_layout(self, at, monkeypatch, cfg, order, rrobin):
         """Per-mode stream (alto_mode_stream): the ALTO stream stably sorted by
         the mode's coordinate — as a whole (order 1, ALTO_MS_ROW_MAJOR) or tile
         by tile (order 0) — cut into tiles of T stored as 8 interleaved slices;
@@ -276,6 +277,7 @@ class TestStreamKernel:
 
         mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
         monkeypatch.setattr(mk, "MS_ORDER", order)
+        monkeypatch.setattr(mk, "MS_RR", rrobin)
         st = synth.make_tensor(self.WIDE if cfg == "wide" else cfg, nnz=60_001)
         dims = st.config.dims
         alto = at.build_alto(at.CooTensor(dims, st.coords, st.values.astype(np.float64)), dtype="float32")
@@ -288,7 +290,7 @@ class TestStreamKernel:
         for mode in range(len(dims)):
             ms = mk.mode_stream(alto, mode)
             assert ms is not None
-            sk, sv, tile = ms
+            sk, sv, tile, rr = ms
             assert tile == T
             sk = sk.cpu().numpy().view(np.uint64).reshape(-1, W)
             sv = sv.cpu().numpy()
@@ -307,7 +309,7 @@ class TestStreamKernel:
             for t0 in list(range(0, alto.nnz, T))[::7] + [alto.nnz - 1 - (alto.nnz - 1) % T]:
                 cnt = min(T, alto.nnz - t0)
                 p = np.arange(cnt)
-                idx = t0 + (p % ch) * 8 + p // ch
+                idx = t0 + (p if rr else (p % ch) * 8 + p // ch)
                 keys = sk[idx]
                 dec = np.stack([(keys[:, fields[n][0]] >> np.uint64(fields[n][1])) & np.uint64((1 << fields[n][2]) - 1)
                                 for n in range(len(dims))], 1).astype(np.int64)

@@ -68,8 +68,9 @@ def main():
             for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] == "mstream"]:
                 del alto._cache[k]
         mk.MS_TILE = tiles[0]
-        for fl, nm in ((-1, "tile-order"),):
+        for fl, nm in ((-1, "tile-order"), (-2, "contiguous-slices")):
             mk.MS_ORDER = 0 if fl == -1 else 1
+            mk.MS_RR = 0 if fl == -2 else 1
             for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] in ("mstream", "hotms")]:
                 del alto._cache[k]
             mk.STREAM_FLAGS = max(fl, 0)
@@ -79,6 +80,7 @@ def main():
             line.append(f"{nm}: {tm:.3f} ms (rel {float((o - ref).norm() / ref.norm()):.1e})")
         mk.STREAM_FLAGS = 0
         mk.MS_ORDER = 1
+        mk.MS_RR = 1
         for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] in ("mstream", "hotms")]:
             del alto._cache[k]
         print("; ".join(line), flush=True)
