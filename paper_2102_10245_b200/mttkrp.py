@@ -387,10 +387,15 @@ def _set_stream(a, ms) -> None:
     a.mkeys, a.mvals, a.mtile, a.mrr = sk.data_ptr(), sv.data_ptr(), st, 1 if rr else 0
 
 
+# Ranks served by the mode-stream kernel (rank 32 stays on the planned kernel
+# unless listed: it measured no faster on cfg3).
+MS_RANKS = tuple(int(x) for x in __import__("os").environ.get("ALTO_MS_RANKS", "16").split(",") if x)
+
+
 def _use_mode_stream(tensor: AltoTensor, rank: int, fbytes: int = 4) -> bool:
-    """Mode-stream kernel: rank 16 (at rank 32 the planned kernel measured faster, cfg3)."""
+    """Mode-stream kernel for the ranks in MS_RANKS."""
     lay = tensor.layout
-    return (MS_TILE > 0 and tensor.nnz > 0 and rank == 16 and 3 <= lay.order <= 5 and max(lay.bits) <= 31
+    return (MS_TILE > 0 and tensor.nnz > 0 and rank in MS_RANKS and 3 <= lay.order <= 5 and max(lay.bits) <= 31
             and tensor.nnz < (1 << 32) - 1 and max(lay.dims) * rank * fbytes < (1 << 32))
 
 
