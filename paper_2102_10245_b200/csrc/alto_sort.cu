@@ -15,7 +15,11 @@
 //      (round j, lane l); __match_any_sync groups equal digits, the group's
 //      lower lanes give the rank, per-warp running digit counters carry the
 //      rank across rounds, and a per-digit exclusive scan over warps orders
-//      the warps.  dest = scan[digit, tile] + warp prefix + rank — stable.
+//      the warps.  The tile is first scattered, stably, into shared memory
+//      in digit order; it is then written out with consecutive threads on
+//      consecutive tile positions, so each digit's run of the tile lands in
+//      consecutive global addresses (scan[digit, tile] + position in run):
+//      coalesced stores instead of one scattered store per key.
 #include <climits>
 
 #include "alto_common.cuh"
@@ -151,6 +155,14 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
                                                               long long ntiles) {
   __shared__ unsigned s_warp[kSortWarps][256];
   __shared__ unsigned s_base[256];
+  __shared__ unsigned s_dstart[256];
+  __shared__ unsigned s_scan[32];
+  extern __shared__ __align__(16) unsigned char s_dyn[];  // digit-sorted tile: keys, then payload
+  uint64_t* s_keys = reinterpret_cast<uint64_t*>(s_dyn);
+  unsigned* s_pay32 = reinterpret_cast<unsigned*>(s_dyn + static_cast<size_t>(kSortTile) * W * 8);
+  uint64_t* s_pay64 = reinterpret_cast<uint64_t*>(s_dyn + static_cast<size_t>(kSortTile) * W * 8);
+  (void)s_pay32;
+  (void)s_pay64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&s_warp[0][0])[i] = 0;
   const long long tile = blockIdx.x;
@@ -185,6 +197,8 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
   }
   __syncthreads();
   {
+    // per-digit exclusive scan over warps (stable order of warps), and the
+    // tile-local exclusive scan over digits (start of digit d's run in the tile)
     const int d = threadIdx.x;
     unsigned run = 0;
 #pragma unroll
@@ -193,18 +207,44 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
       s_warp[w][d] = run;
       run += c;
     }
+    unsigned total;
+    s_dstart[d] = block_exclusive_scan(run, s_scan, &total);
   }
   __syncthreads();
+  // 1) stable local scatter into shared memory (digit-sorted tile)
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const long long i = base + j * 32 + lane;
     if (i < m) {
       const unsigned d = dig[j];
-      const long long dst = static_cast<long long>(s_base[d]) + s_warp[warp][d] + rank[j];
-      store_key<W>(keys_out, dst, k[j]);
-      if constexpr (P == 4) static_cast<unsigned*>(pay_out)[dst] = static_cast<unsigned>(pv[j]);
-      if constexpr (P == 8) static_cast<uint64_t*>(pay_out)[dst] = pv[j];
+      const unsigned lp = s_dstart[d] + s_warp[warp][d] + rank[j];
+      if constexpr (W == 1) {
+        s_keys[lp] = k[j].w[0];
+      } else {
+        s_keys[2 * lp] = k[j].w[0];
+        s_keys[2 * lp + 1] = k[j].w[1];
+      }
+      if constexpr (P == 4) s_pay32[lp] = static_cast<unsigned>(pv[j]);
+      if constexpr (P == 8) s_pay64[lp] = pv[j];
     }
+  }
+  __syncthreads();
+  // 2) coalesced write-out: consecutive tile positions of one digit go to
+  //    consecutive global positions
+  const int cnt = static_cast<int>(min(static_cast<long long>(kSortTile), m - tile * kSortTile));
+  for (int lp = threadIdx.x; lp < cnt; lp += kSortThreads) {
+    Key<W> key;
+    if constexpr (W == 1) {
+      key.w[0] = s_keys[lp];
+    } else {
+      key.w[0] = s_keys[2 * lp];
+      key.w[1] = s_keys[2 * lp + 1];
+    }
+    const unsigned d = digit_of<W>(key, shift);
+    const long long dst = static_cast<long long>(s_base[d]) + (lp - s_dstart[d]);
+    store_key<W>(keys_out, dst, key);
+    if constexpr (P == 4) static_cast<unsigned*>(pay_out)[dst] = s_pay32[lp];
+    if constexpr (P == 8) static_cast<uint64_t*>(pay_out)[dst] = s_pay64[lp];
   }
 }
 
@@ -262,6 +302,13 @@ static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, con
   const long long ncounts = 256 * ntiles;
   const long long nparts = (ncounts + kScanChunk - 1) / kScanChunk;
   const int passes = (total_bits + 7) / 8;
+  const size_t smem = static_cast<size_t>(kSortTile) * (W * 8 + P);
+  static bool attr_set = false;
+  if (!attr_set) {
+    ALTO_CUDA_TRY(cudaFuncSetAttribute(radix_scatter<W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    attr_set = true;
+  }
   uint64_t* kin = keys;
   uint64_t* kout = ws.keys_alt;
   void* pin = pay;
@@ -272,8 +319,8 @@ static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, con
     scan_reduce<<<static_cast<unsigned>(nparts), kScanThreads, 0, s>>>(ws.counts, ncounts, ws.partial);
     scan_partials<<<1, 1024, 0, s>>>(ws.partial, nparts);
     scan_down<<<static_cast<unsigned>(nparts), kScanThreads, 0, s>>>(ws.counts, ncounts, ws.partial);
-    radix_scatter<W, P><<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, pin, kout, pout, m, shift,
-                                                                              ws.counts, ntiles);
+    radix_scatter<W, P><<<static_cast<unsigned>(ntiles), kSortThreads, smem, s>>>(kin, pin, kout, pout, m, shift,
+                                                                                 ws.counts, ntiles);
     std::swap(kin, kout);
     std::swap(pin, pout);
   }
