@@ -211,10 +211,19 @@ def run_b200(args):
     from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
 
     ws, rank, local = dist_env()
+    # functional check of the multi-rank path on a one-GPU box only
+    # (ALTO_BENCH_TEST_GLOO=1: every rank on cuda:0, gloo collectives; numbers
+    # from such a run are not measurements)
+    test_gloo = os.environ.get("ALTO_BENCH_TEST_GLOO") == "1"
+    if test_gloo:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if test_gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = synth.CONFIGS[args.config]
     nnz_total = args.nnz or cfg.nnz
     t_gen = time.time()
