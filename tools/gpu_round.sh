@@ -11,5 +11,3 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mstream_kernel --launch-skip 6 -c 3 -o gpurun_out/mstream_full -f python bench.py --steps 3 --warmup 3 --skip-cpu --skip-cpals > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"
 for c in 1 3 4; do timeout 900 python bench.py --config $c --steps 10 > gpurun_out/bench_cfg$c.log 2>&1; echo "cfg$c rc=$?"; tail -1 gpurun_out/bench_cfg$c.log | cut -c1-300; done
 timeout 1800 python bench.py --config 5 --steps 5 --cpu-sample 1000000 > gpurun_out/bench_cfg5.log 2>&1; echo "cfg5 rc=$?"; tail -1 gpurun_out/bench_cfg5.log | cut -c1-300
-timeout 600 python tools/ab_mstream.py 2 0 1024 2048 2>&1 | tail -4
-timeout 900 python tools/ab_mstream.py 5 0 1024 2>&1 | tail -4

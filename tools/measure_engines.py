@@ -1,6 +1,6 @@
 """Ad-hoc measurements used for DESIGN.md (not part of the product):
-  python tools_measure.py exact  [nnz]      exact-order engine vs streaming on the cfg2 law
-  python tools_measure.py cpals5 [nnz] [it]  CP-ALS on the cfg5 law (128-bit keys)"""
+  python tools/measure_engines.py exact  [nnz]      exact-order engine vs streaming on the cfg2 law
+  python tools/measure_engines.py cpals5 [nnz] [it]  CP-ALS on the cfg5 law (128-bit keys)"""
 import sys
 import time
 
