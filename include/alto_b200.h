@@ -249,7 +249,7 @@ int alto_subtile_order(const alto_layout* lay, const uint64_t* packed, int64_t m
  * 64*n_words-1 set on elements of hot rows.  Returns ALTO_EUNSUPPORTED when
  * that layout does not fit below bit 64*n_words-1.  skeys / svals
  * hold ceil(m/tile)*tile elements (the tail is zero padding).  value_dtype
- * ALTO_F32 or ALTO_F64; tile a multiple of 256 with m / tile < 2^31. */
+ * ALTO_F32 or ALTO_F64; tile a multiple of 128 with m / tile < 2^31. */
 size_t alto_mode_stream_workspace_bytes(int64_t m);
 #define ALTO_MS_ROW_MAJOR 1 /* flags: sort the whole stream by the mode's coordinate (stable: ALTO order
                                within a row), not tile by tile */

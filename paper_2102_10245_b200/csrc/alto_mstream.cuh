@@ -125,7 +125,7 @@ __device__ __forceinline__ unsigned ms_field(const Key<W>& k, const FSel& f) {
 struct MStream {
   const uint64_t* keys;  // (ntiles*T, W) stream keys (MsFields layout), hot flag in bit 64W-1
   const void* vals;      // (ntiles*T,) values
-  int tile;              // T (multiple of 256)
+  int tile;              // T (multiple of 128)
   MsFields f;
   int rr;                // round-robin slices: group s takes sorted positions s, s+8, ...
 };

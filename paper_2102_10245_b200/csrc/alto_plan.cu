@@ -196,7 +196,7 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
   ALTO_REQUIRE(mode >= 0 && mode < lay->order, "mode out of range");
   ALTO_REQUIRE(lay->bits[mode] <= 31, "mode stream needs mode extents below 2^31");
   ALTO_REQUIRE(value_dtype == ALTO_F32 || value_dtype == ALTO_F64, "unsupported value dtype");
-  ALTO_REQUIRE(tile >= 256 && tile % 256 == 0, "tile must be a positive multiple of 256");
+  ALTO_REQUIRE(tile >= 128 && tile % 128 == 0, "tile must be a positive multiple of 128");
   ALTO_REQUIRE(m >= 0 && m < (1ll << 32) - 1, "mode stream supports fewer than 2^32 elements");
   const DevLayout d = make_dev_layout(lay);
   const MsFields F = ms_fields(d, mode);

@@ -168,8 +168,8 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.mvals = a->mvals;
   P.mtile = a->mtile;
   P.mrr = a->mrr;
-  ALTO_REQUIRE(!a->mkeys || (a->mvals && a->mtile >= 256 && a->mtile % 256 == 0),
-               "mode stream needs values and a tile that is a multiple of 256");
+  ALTO_REQUIRE(!a->mkeys || (a->mvals && a->mtile >= 128 && a->mtile % 128 == 0),
+               "mode stream needs values and a tile that is a multiple of 128");
   ALTO_REQUIRE(!a->mkeys || a->n_hot <= 0 || a->hot_base, "mode-stream hot plan needs hot_base");
   ALTO_REQUIRE(!a->mkeys || a->rank <= 32, "the mode-stream hot-row reduction supports ranks up to 32");
   Plan2 pl2{};
@@ -244,7 +244,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
 int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_hot, int64_t m, int32_t tile,
                     int32_t flags, int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base,
                     void* stream) {
-  ALTO_REQUIRE(n_hot >= 0 && tile >= 256 && bound >= 1 && max_lg >= 0 && max_lg <= 20, "bad hot copy plan arguments");
+  ALTO_REQUIRE(n_hot >= 0 && tile >= 128 && bound >= 1 && max_lg >= 0 && max_lg <= 20, "bad hot copy plan arguments");
   ALTO_REQUIRE(static_cast<long long>(n_hot) << max_lg < (1ll << 26), "too many hot-row copies");
   if (n_hot == 0) return ALTO_OK;
   cudaStream_t s = as_stream(stream);

@@ -337,11 +337,11 @@ MS_RR = int(__import__("os").environ.get("ALTO_MS_RR", 1))
 
 
 def ms_tile(tensor: AltoTensor) -> int:
-    """Tile length of the tensor's mode streams: MS_TILE, shrunk (to 512 or
-    256) for small tensors so that there are >= ~4 tiles per resident warp
+    """Tile length of the tensor's mode streams: MS_TILE, halved (down to 128)
+    for small tensors so that there are >= ~4 tiles per resident warp
     (148 SMs x 24 warps)."""
     t = MS_TILE
-    while t > 256 and tensor.nnz < 148 * 24 * 4 * t:
+    while t > 128 and tensor.nnz < 148 * 24 * 4 * t:
         t //= 2
     return t
 

@@ -286,7 +286,7 @@ class TestStreamKernel:
         coords = orc.decode(orc.build_layout(dims), alto.indices)
         vals = alto.vals.cpu().numpy()
         T = mk.ms_tile(alto)
-        assert T == 256  # small tensor: shortest tiles
+        assert T == 128  # small tensor: shortest tiles
         for mode in range(len(dims)):
             ms = mk.mode_stream(alto, mode)
             assert ms is not None
