@@ -68,6 +68,13 @@ def main():
             for k in [k for k in alto._cache if isinstance(k, tuple) and k[0] == "mstream"]:
                 del alto._cache[k]
         mk.MS_TILE = tiles[0]
+        for fl in [int(x) for x in __import__("os").environ.get("AB_FLAGS", "").split(",") if x]:
+            mk.STREAM_FLAGS = fl
+            o = mttkrp_stream(alto, f, mode, out_dtype=fd)
+            tm = timed(lambda: mttkrp_stream(alto, f, mode, out=o, out_dtype=fd), flush=flush)
+            o = mttkrp_stream(alto, f, mode, out_dtype=fd).double()
+            line.append(f"flags {fl}: {tm:.3f} ms (rel {float((o - ref).norm() / ref.norm()):.1e})")
+        mk.STREAM_FLAGS = 0
         for fl, nm in ((-1, "tile-order"), (-2, "contiguous-slices")):
             mk.MS_ORDER = 0 if fl == -1 else 1
             mk.MS_RR = 0 if fl == -2 else 1
