@@ -338,6 +338,8 @@ def run_b200(args):
     launches_per_step = 0
     for n in range(N):
         launches_per_step += 1
+        if ms_used and alto.vals.dtype == torch.float32:
+            launches_per_step += len(mk.ms_pairs(dims, n, R, 4))  # alto_krp_pair tables
         if not args.no_hot:
             hp = (alto._cache.get(("hotms", n, R, odt, mk.ms_tile(alto), mk.MS_ORDER)) if ms_used
                   else alto._cache.get(("hot", n, R, odt)))

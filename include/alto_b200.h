@@ -194,7 +194,23 @@ typedef struct alto_mttkrp_args {
    * elements of out_dtype (zero on entry, left zero). */
   const int32_t* hot_base;
   int32_t mrr;                   /* mode stream built with ALTO_MS_ROUND_ROBIN */
+  /* Paired input modes (mode stream only; float32 values and factors, rank
+   * 16, orders 4-5): input modes pair_a[i], pair_b[i] (i < n_pairs, disjoint,
+   * not `mode`) are gathered together as one row of pair_tab[i], the
+   * row-wise product table of their factors (alto_krp_pair: row
+   * ia * I_b + ib), so one gather replaces two.  I_a * I_b * rank * 4 must
+   * stay below 2^32 bytes; ALTO_EUNSUPPORTED otherwise. */
+  int32_t n_pairs;
+  int32_t pair_a[2];
+  int32_t pair_b[2];
+  const void* pair_tab[2];
 } alto_mttkrp_args;
+
+/* Row-wise (Khatri-Rao) product table of two factors for paired input modes:
+ * out[ia * rows_b + ib][r] = fa[ia][r] * fb[ib][r], (rows_a * rows_b, rank)
+ * row-major, dtype ALTO_F32 or ALTO_F64. */
+int alto_krp_pair(const void* fa, int64_t rows_a, const void* fb, int64_t rows_b, int32_t rank, int32_t dtype,
+                  void* out, void* stream);
 
 /* Deterministic MTTKRP support (ALTO_I64 output).  alto_sumabs / alto_absmax:
  * float64 sum of |x| / max |x| (fixed-order two-stage reductions, `ws` from

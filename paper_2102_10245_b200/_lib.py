@@ -67,6 +67,10 @@ class CMttkrpArgs(Structure):
         ("mtile", c_int32),
         ("hot_base", c_void_p),
         ("mrr", c_int32),
+        ("n_pairs", c_int32),
+        ("pair_a", c_int32 * 2),
+        ("pair_b", c_int32 * 2),
+        ("pair_tab", c_void_p * 2),
     ]
 
 
@@ -127,6 +131,7 @@ SIGNATURES = [
     ("alto_sumsq", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_cast_f64_f32", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
     ("alto_cast_f32_f64", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+    ("alto_krp_pair", c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     ("alto_sumabs", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_absmax", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_fixed_scale", c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),

@@ -122,16 +122,26 @@ __device__ __forceinline__ unsigned ms_field(const Key<W>& k, const FSel& f) {
   return static_cast<unsigned>(w >> f.sh) & f.mask;
 }
 
+// One gathered input of the mode-stream kernel: a factor (nb < 0) or, for a
+// pair of input modes (na, nb), the row-wise product table of their factors
+// with row ia * db + ib (alto_krp_pair), so one gather serves both modes.
+struct VIn {
+  const void* tab;
+  int na, nb;
+  unsigned db;
+};
+
 struct MStream {
   const uint64_t* keys;  // (ntiles*T, W) stream keys (MsFields layout), hot flag in bit 64W-1
   const void* vals;      // (ntiles*T,) values
   int tile;              // T (multiple of 128)
   MsFields f;
   int rr;                // round-robin slices: group s takes sorted positions s, s+8, ...
+  VIn vin[ALTO_MAX_ORDER];  // gathered inputs when input modes are paired (P.n_pairs > 0)
 };
 
 template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, bool COOP = false,
-          bool XCH_SHFL = false, bool XKEY = false>
+          bool XCH_SHFL = false, bool XKEY = false, int NV = N - 1>
 __global__ void __launch_bounds__(kTileThreads, MINB)
 mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStream S,
                const __grid_constant__ StreamParams P) {
@@ -140,7 +150,8 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
   constexpr int G = R / 4;          // lanes per element
   constexpr int GPW = 32 / G;       // slices processed at once by a warp
   constexpr int PASSES = kMsSlices / GPW;
-  constexpr int NIN = N - 1;
+  constexpr int NIN = NV;            // gathered inputs (N-1, or fewer with paired modes)
+  constexpr bool PAIR = NV < N - 1;
   constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
   constexpr unsigned HOTF = 0x80000000u;
   static_assert(!COOP || (U >= 1 && U <= G), "one decoding lane per element of a block");
@@ -156,14 +167,30 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
   const int gl = lane % G;
   const unsigned qmask = (G >= 4) ? (0xFu << (lane & ~3)) : 0xffffffffu;
   const char* fin_lane[NIN];
+  FSel fin[NIN];
+  FSel finb[PAIR ? NIN : 1];
+  unsigned vdb[PAIR ? NIN : 1];
 #pragma unroll
   for (int k = 0; k < NIN; ++k) {
-    const int n = k < mode ? k : k + 1;
-    fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(P.factors[n]) + 4 * gl);
+    if constexpr (PAIR) {
+      const VIn& vi = S.vin[k];
+      fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(vi.tab) + 4 * gl);
+      fin[k] = fsel_of(S.f, vi.na);
+      finb[k] = vi.nb >= 0 ? fsel_of(S.f, vi.nb) : FSel{0u, 0u, false};  // empty field reads 0
+      vdb[k] = vi.nb >= 0 ? vi.db : 1u;
+    } else {
+      const int n = k < mode ? k : k + 1;
+      fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(P.factors[n]) + 4 * gl);
+      fin[k] = fsel_of(S.f, n);
+    }
   }
-  FSel fin[NIN];
-#pragma unroll
-  for (int k = 0; k < NIN; ++k) fin[k] = fsel_of(S.f, k < mode ? k : k + 1);
+  // byte offset of input k's gathered row for key kk
+  auto voff = [&](const Key<W>& kk, int k) -> unsigned {
+    if constexpr (PAIR)
+      return (ms_field<W>(kk, fin[k]) * vdb[k] + ms_field<W>(kk, finb[k])) * ROWB;
+    else
+      return ms_field<W>(kk, fin[k]) * ROWB;
+  };
   const FSel fout = fsel_of(S.f, mode);
   const V* __restrict__ vals = static_cast<const V*>(S.vals);
   O* __restrict__ out = static_cast<O*>(P.out);
@@ -262,7 +289,7 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
             for (int u = 0; u < U; ++u)
               if (FULL || j0 + u < len)
 #pragma unroll
-                for (int k = 0; k < NIN; ++k) g[u][k] = gather_off<F>(fin_lane[k], ms_field<W>(kk[u], fin[k]) * ROWB);
+                for (int k = 0; k < NIN; ++k) g[u][k] = gather_off<F>(fin_lane[k], voff(kk[u], k));
 #pragma unroll
             for (int u = 0; u < U; ++u)
               if (FULL || j0 + u < len) consume(target(kk[u]), vv[u], g[u]);
@@ -297,7 +324,7 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
           prefetch(j0 + U);
           unsigned moff[NIN];
 #pragma unroll
-          for (int k = 0; k < NIN; ++k) moff[k] = ms_field<W>(kk, fin[k]) * ROWB;
+          for (int k = 0; k < NIN; ++k) moff[k] = voff(kk, k);
           const unsigned mtg = (gl < U && j0 + gl < len) ? target(kk) : 0xffffffffu;
           V4<F> g[U][NIN];
           unsigned tg[U];
@@ -319,7 +346,7 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
               tg[u] = j0 + u < len ? target(ku) : 0xffffffffu;
 #pragma unroll
               for (int k = 0; k < NIN; ++k)
-                if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], ms_field<W>(ku, fin[k]) * ROWB);
+                if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], voff(ku, k));
             }
           } else if constexpr (XCH_SHFL) {
 #pragma unroll
@@ -394,9 +421,9 @@ constexpr int ms_u() {
 }
 
 template <int W, typename V, typename O, int N, int R, bool COOP = true, int MINB = 3,
-          int U = ms_u<N, R, V, (COOP ? 32 : 16), COOP>(), bool XCH_SHFL = true, bool XKEY = false>
+          int U = ms_u<N, R, V, (COOP ? 32 : 16), COOP>(), bool XCH_SHFL = true, bool XKEY = false, int NV = N - 1>
 int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, cudaStream_t s) {
-  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, COOP, XCH_SHFL, XKEY>;
+  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, COOP, XCH_SHFL, XKEY, NV>;
   static int cached_bps = 0;
   if (!cached_bps) {
     int b = 1;
@@ -420,8 +447,30 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
   if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
   for (int n = 0; n < d.order; ++n)
     if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
-  const MStream S{P.mkeys, P.mvals, P.mtile, ms_fields(d, P.mode), P.mrr};
+  MStream S{P.mkeys, P.mvals, P.mtile, ms_fields(d, P.mode), P.mrr, {}};
   if (!S.f.ok) return ALTO_EUNSUPPORTED;
+  if (P.n_pairs > 0) {
+    // paired input modes (alto_krp_pair tables): float32 data, rank 16, orders 4-5
+    if constexpr (sizeof(V) == 4 && !std::is_same<O, long long>::value) {
+      if (P.rank != 16 || d.order < 4) return ALTO_EUNSUPPORTED;
+      int nv = 0;
+      unsigned used = 1u << P.mode;
+      for (int i = 0; i < P.n_pairs; ++i) {
+        const int a = P.pair_a[i], b = P.pair_b[i];
+        if (a < 0 || b < 0 || a >= d.order || b >= d.order || a == b || ((used >> a) & 1u) || ((used >> b) & 1u) ||
+            !P.pair_tab[i] || d.dims[a] * d.dims[b] * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll)
+          return ALTO_EUNSUPPORTED;
+        used |= (1u << a) | (1u << b);
+        S.vin[nv++] = VIn{P.pair_tab[i], a, b, static_cast<unsigned>(d.dims[b])};
+      }
+      for (int n = 0; n < d.order; ++n)
+        if (!((used >> n) & 1u)) S.vin[nv++] = VIn{P.factors[n], n, -1, 1u};
+      if (d.order == 4 && nv == 2) return launch_mstream<W, V, O, 4, 16, true, 3, ms_u<3, 16, V, 32, true>(), true, false, 2>(d, S, P, s);
+      if (d.order == 5 && nv == 3) return launch_mstream<W, V, O, 5, 16, true, 3, ms_u<4, 16, V, 32, true>(), true, false, 3>(d, S, P, s);
+      if (d.order == 5 && nv == 2) return launch_mstream<W, V, O, 5, 16, true, 3, ms_u<3, 16, V, 32, true>(), true, false, 2>(d, S, P, s);
+    }
+    return ALTO_EUNSUPPORTED;
+  }
   if constexpr (W == 1 && sizeof(V) == 4 && sizeof(O) == 4) {
     // tuning variants for the cfg2 shape (A/B only)
     if (d.order == 3 && P.rank == 16) {

@@ -168,6 +168,13 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.mvals = a->mvals;
   P.mtile = a->mtile;
   P.mrr = a->mrr;
+  P.n_pairs = (a->mkeys && a->out_dtype != ALTO_I64) ? std::max(0, std::min(a->n_pairs, 2)) : 0;
+  ALTO_REQUIRE(a->n_pairs <= 2, "at most 2 paired input modes");
+  for (int i = 0; i < 2; ++i) {
+    P.pair_a[i] = a->pair_a[i];
+    P.pair_b[i] = a->pair_b[i];
+    P.pair_tab[i] = a->pair_tab[i];
+  }
   ALTO_REQUIRE(!a->mkeys || (a->mvals && a->mtile >= 128 && a->mtile % 128 == 0),
                "mode stream needs values and a tile that is a multiple of 128");
   ALTO_REQUIRE(!a->mkeys || a->n_hot <= 0 || a->hot_base, "mode-stream hot plan needs hot_base");
@@ -321,3 +328,48 @@ int alto_unpack_rows(void* dst, int32_t dtype, const int64_t* rows, int64_t n, i
   return ALTO_OK;
 }
 }  // extern "C"
+
+// ---- paired input modes: row-wise product table (mode-stream gathers) --------
+namespace alto {
+// out[ia * rb + ib][r] = fa[ia][r] * fb[ib][r]; VEC elements per thread
+// (float4 stores for float32 when rank % 4 == 0).
+template <typename T, int VEC>
+__global__ void krp_pair_kernel(const T* __restrict__ fa, const T* __restrict__ fb, long long rb, int R,
+                                long long total, T* __restrict__ out) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i * VEC < total; i += stride) {
+    const long long e = i * VEC;
+    const long long row = e / R;
+    const int r = static_cast<int>(e - row * R);
+    const long long ia = row / rb, ib = row - ia * rb;
+    if constexpr (VEC == 4) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(fa + ia * R + r));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(fb + ib * R + r));
+      reinterpret_cast<float4*>(out)[i] = make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w);
+    } else {
+      out[e] = fa[ia * R + r] * fb[ib * R + r];
+    }
+  }
+}
+}  // namespace alto
+
+extern "C" int alto_krp_pair(const void* fa, int64_t rows_a, const void* fb, int64_t rows_b, int32_t rank,
+                             int32_t dtype, void* out, void* stream) {
+  ALTO_REQUIRE(rank >= 1 && rows_a >= 0 && rows_b >= 0, "bad table shape");
+  ALTO_REQUIRE(dtype == ALTO_F32 || dtype == ALTO_F64, "unsupported dtype");
+  const long long total = static_cast<long long>(rows_a) * rows_b * rank;
+  if (total <= 0) return ALTO_OK;
+  cudaStream_t s = as_stream(stream);
+  if (dtype == ALTO_F32 && rank % 4 == 0)
+    krp_pair_kernel<float, 4><<<grid_for(total / 4, 256, kSMs * 8), 256, 0, s>>>(
+        static_cast<const float*>(fa), static_cast<const float*>(fb), rows_b, rank, total, static_cast<float*>(out));
+  else if (dtype == ALTO_F32)
+    krp_pair_kernel<float, 1><<<grid_for(total, 256, kSMs * 8), 256, 0, s>>>(
+        static_cast<const float*>(fa), static_cast<const float*>(fb), rows_b, rank, total, static_cast<float*>(out));
+  else
+    krp_pair_kernel<double, 1><<<grid_for(total, 256, kSMs * 8), 256, 0, s>>>(
+        static_cast<const double*>(fa), static_cast<const double*>(fb), rows_b, rank, total,
+        static_cast<double*>(out));
+  ALTO_LAUNCH_CHECK("alto_krp_pair");
+  return ALTO_OK;
+}

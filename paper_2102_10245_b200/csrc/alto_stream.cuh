@@ -66,6 +66,9 @@ struct StreamParams {
   const void* mvals;          //   values
   int mtile;                  //   tile length T
   int mrr;                    //   round-robin slices (ALTO_MS_ROUND_ROBIN)
+  int n_pairs;                // paired input modes (mode stream): count,
+  int pair_a[2], pair_b[2];   //   modes,
+  const void* pair_tab[2];    //   row-wise product tables (alto_krp_pair)
   const double* fixed_scale;  // deterministic mode: device scalar, int64 output = round(x * scale)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
 };
 

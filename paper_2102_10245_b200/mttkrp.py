@@ -392,6 +392,50 @@ def _set_stream(a, ms) -> None:
 MS_RANKS = tuple(int(x) for x in __import__("os").environ.get("ALTO_MS_RANKS", "16").split(",") if x)
 
 
+# Paired input modes (orders 4-5, float32, rank 16): two input modes whose
+# row-wise product table (I_a * I_b rows) stays within MS_PAIR_BYTES are
+# gathered as one row, so one gather replaces two (0 disables pairing).
+MS_PAIR_BYTES = int(__import__("os").environ.get("ALTO_MS_PAIR_BYTES", 64 << 20))
+
+
+def ms_pairs(dims, mode: int, rank: int, fbytes: int = 4, limit: int | None = None):
+    """Input-mode pairs for the mode-stream kernel: the two smallest input
+    modes, then the next two, while each pair's product table fits `limit`
+    bytes (at most 2 pairs; orders 4-5, rank 16, float32 only)."""
+    limit = MS_PAIR_BYTES if limit is None else limit
+    if limit <= 0 or rank != 16 or fbytes != 4 or not 4 <= len(dims) <= 5:
+        return []
+    ins = sorted((n for n in range(len(dims)) if n != mode), key=lambda n: (dims[n], n))
+    pairs = []
+    for i in range(0, len(ins) - 1, 2):
+        a, b = ins[i], ins[i + 1]
+        if dims[a] * dims[b] * rank * fbytes > min(limit, (1 << 32) - 1):
+            break
+        pairs.append((a, b))
+    return pairs
+
+
+def _set_pairs(a, tensor: AltoTensor, fdev: list, mode: int, keep: list) -> None:
+    """Build the product tables of the paired input modes (alto_krp_pair) and
+    hand them to the mode-stream kernel."""
+    torch = _torch()
+    rank = int(fdev[0].shape[1])
+    if tensor.vals.dtype != torch.float32 or fdev[0].dtype != torch.float32:
+        return
+    pairs = ms_pairs(tensor.layout.dims, mode, rank, 4)
+    if not pairs:
+        return
+    lib = _lib.load()
+    for i, (pa, pb) in enumerate(pairs):
+        da, db = tensor.layout.dims[pa], tensor.layout.dims[pb]
+        tab = torch.empty((da * db, rank), dtype=torch.float32, device=fdev[0].device)
+        _lib.check(lib.alto_krp_pair(fdev[pa].data_ptr(), da, fdev[pb].data_ptr(), db, rank, _lib.ALTO_F32,
+                                     tab.data_ptr(), _lib.stream_ptr()), "alto_krp_pair")
+        keep.append(tab)
+        a.pair_a[i], a.pair_b[i], a.pair_tab[i] = pa, pb, tab.data_ptr()
+    a.n_pairs = len(pairs)
+
+
 def _use_mode_stream(tensor: AltoTensor, rank: int, fbytes: int = 4) -> bool:
     """Mode-stream kernel for the ranks in MS_RANKS."""
     lay = tensor.layout
@@ -455,6 +499,8 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
           and _use_mode_stream(tensor, rank, fdev[0].element_size()) else None)
     if ms is not None:
         _set_stream(a, ms)
+        tabs = []  # product tables: stream-ordered, released after the launch
+        _set_pairs(a, tensor, fdev, mode, tabs)
     elif planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
             and max(tensor.layout.bits) <= 31:
         a.packed = packed_keys(tensor).data_ptr()

@@ -329,6 +329,43 @@ class TestStreamKernel:
             assert rel_error(a, b) <= 1e-6
             torch.cuda.synchronize()
 
+    @pytest.mark.parametrize("cfg", [4, "four"])
+    def test_paired_input_modes(self, at, monkeypatch, cfg):
+        """Paired input modes (alto_krp_pair tables, one gather for two modes):
+        every mode against the float64 oracle and the unpaired kernel, plus
+        the product table itself against NumPy."""
+        import importlib
+
+        import torch
+
+        mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+        four = synth.SynthConfig("cfg8", (3000, 700, 40, 90), 0, (("zipf", 1.1),) * 2 + (("uniform", 0),) * 2,
+                                 "uniform01", "float32", 16)
+        st = synth.make_tensor(four if cfg == "four" else cfg, nnz=120_007)
+        dims = st.config.dims
+        coo = at.CooTensor(dims, st.coords, st.values.astype(np.float32).astype(np.float64))
+        alto = at.build_alto(coo, dtype="float32")
+        rng = np.random.default_rng(5)
+        f32 = [rng.random((d, 16)).astype(np.float32) for d in dims]
+        fdev = mk.factors_to_device(f32)
+        for mode in range(len(dims)):
+            pairs = mk.ms_pairs(dims, mode, 16, 4)
+            assert pairs, (dims, mode)
+            ref = orc.mttkrp_coo(st.coords, coo.values, [f.astype(np.float64) for f in f32], mode)
+            a = mk.mttkrp_stream(alto, fdev, mode).cpu().numpy()
+            monkeypatch.setattr(mk, "MS_PAIR_BYTES", 0)
+            b = mk.mttkrp_stream(alto, fdev, mode).cpu().numpy()
+            monkeypatch.setattr(mk, "MS_PAIR_BYTES", 64 << 20)
+            assert rel_error(a, ref) <= 1e-5
+            assert rel_error(a, b) <= 1e-6
+        pa, pb = mk.ms_pairs(dims, 0, 16, 4)[0]
+        tab = torch.empty((dims[pa] * dims[pb], 16), dtype=torch.float32, device="cuda")
+        from paper_2102_10245_b200 import _lib
+        _lib.check(_lib.load().alto_krp_pair(fdev[pa].data_ptr(), dims[pa], fdev[pb].data_ptr(), dims[pb], 16,
+                                             _lib.ALTO_F32, tab.data_ptr(), _lib.stream_ptr()), "alto_krp_pair")
+        want = (f32[pa][:, None, :] * f32[pb][None, :, :]).reshape(-1, 16)
+        assert np.array_equal(tab.cpu().numpy(), want)
+
     def test_hot_copy_plan(self, at):
         """alto_hot_copies: per hot row 2^lg copies with 2^lg * HOT_BOUND >=
         estimated merges (lg <= HOT_MAX_LG), laid out slot by slot."""

@@ -157,6 +157,31 @@ class TestSynth:
         assert len(np.unique(t.coords, axis=0)) == 5_000
 
 
+class TestModeStreamPairs:
+    """ms_pairs: which input modes the mode-stream kernel gathers as one
+    product-table row (smallest two, then the next two, within the byte cap)."""
+
+    def test_cfg4_pairs(self):
+        import importlib
+
+        mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+        dims = synth.CONFIGS[4].dims  # 1000 x 1000 x 1000 x 100 x 50
+        assert mk.ms_pairs(dims, 0, 16, 4, 64 << 20) == [(4, 3), (1, 2)]
+        assert mk.ms_pairs(dims, 3, 16, 4, 64 << 20) == [(4, 0), (1, 2)]
+        assert mk.ms_pairs(dims, 0, 16, 4, 1 << 20) == [(4, 3)]  # 5000 rows x 64 B fit, 1M rows do not
+
+    def test_not_paired(self):
+        import importlib
+
+        mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+        assert mk.ms_pairs(synth.CONFIGS[2].dims, 0, 16, 4, 64 << 20) == []  # order 3
+        assert mk.ms_pairs(synth.CONFIGS[4].dims, 0, 32, 4, 64 << 20) == []  # rank 32
+        assert mk.ms_pairs(synth.CONFIGS[4].dims, 0, 16, 8, 64 << 20) == []  # float64
+        assert mk.ms_pairs(synth.CONFIGS[4].dims, 0, 16, 4, 0) == []  # disabled
+        assert mk.ms_pairs(synth.CONFIGS[3].dims, 0, 16, 4, 64 << 20) == [(3, 2)]  # 2000 x 500 x 64 B = 64e6 B
+        assert mk.ms_pairs(synth.CONFIGS[3].dims, 0, 16, 4, 64_000_000 - 1) == []
+
+
 class TestBenchContract:
     """bench.py's reference arm (CPU only) prints one JSON line with the
     contract's keys; the argument parser accepts every documented flag."""
