@@ -686,9 +686,18 @@ def mttkrp_seq(tensor: AltoTensor, factors, mode: int):
 
 
 def _any_flag(tensor: AltoTensor, flag_bit: int) -> bool:
+    """Whether any element carries `flag_bit` (the reference's `flags.any()`
+    guard, mttkrp.py:192-200).  The answer is cached on the tensor (its keys
+    are read-only; flagging returns a new tensor), so repeated calls do not
+    re-read the keys or synchronize the host with the device."""
     if tensor.nnz == 0:
         return False
-    return bool(read_flags_device(tensor, flag_bit).any().item())
+    key = ("anyflag", flag_bit)
+    hit = tensor._cache.get(key)
+    if hit is None:
+        hit = bool(read_flags_device(tensor, flag_bit).any().item())
+        tensor._cache[key] = hit
+    return hit
 
 
 def mttkrp_par(tensor: AltoTensor, parts: PartitionSet, plan: ConflictPlan, factors, mode: int,

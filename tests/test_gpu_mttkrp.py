@@ -115,6 +115,15 @@ class TestParallelSemantics:
         assert any(plan.overlaps)
         with pytest.raises(ValueError, match="flags"):
             at.mttkrp_par(alto, parts, plan, factors, 0, workers=2)
+        # the guard's answer is cached per tensor: still raises on repeat,
+        # and a flagged tensor passes it on every call
+        with pytest.raises(ValueError, match="flags"):
+            at.mttkrp_par(alto, parts, plan, factors, 0, workers=2)
+        flagged = at.apply_boundary_flags(alto, plan)
+        a = at.mttkrp_par(flagged, parts, plan, factors, 0, workers=2)
+        b = at.mttkrp_par(flagged, parts, plan, factors, 0, workers=2)
+        assert ("anyflag", plan.flag_bit) in flagged._cache
+        assert rel_error(a, b) <= 1e-12
 
     def test_plan_mismatch(self, at, setup):
         _, alto, factors = setup
