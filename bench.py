@@ -99,30 +99,83 @@ def bytes_alg(dims, nnz, key_bytes, val_bytes, rank, fbytes, mode):
 
 
 def cpu_baseline_sample(cfg_id: int, sample_nnz: int, threads: int, reps: int = 3):
-    """The reference algorithm (oracle port of mttkrp_par, Buffered = the
-    reference's auto choice for cfg2) on a bounded same-law sample, all modes."""
-    from oracle import alto_oracle as orc
+    """The reference's CPU MTTKRP (installed reference when present, else the
+    oracle port of Buffered mttkrp_par) on a bounded same-law sample, all modes."""
     from paper_2102_10245_b200 import synth
 
-    st = synth.make_tensor(cfg_id, nnz=sample_nnz)
-    c = st.config
-    lay = orc.build_layout(c.dims)
-    words, vals = orc.build(lay, st.coords, st.values.astype(np.float64))
-    rng = np.random.default_rng(synth.SEED_FACTOR_BASE + cfg_id)
-    factors = [rng.random((d, c.rank)).astype(np.float32).astype(np.float64) for d in c.dims]
-    offs, iv, _ = orc.partition(lay, words, threads)
+    c = synth.CONFIGS[cfg_id]
+    step, kind, what = reference_step(cfg_id, sample_nnz, threads)
     times = []
     for _rep in range(reps + 1):
         t0 = time.perf_counter()
-        for mode in range(len(c.dims)):
-            orc.mttkrp_buffered(lay, words, vals, factors, mode, offs, iv, workers=threads)
+        step()
         times.append(time.perf_counter() - t0)
     t = sum(times[1:]) / reps  # first rep is warm-up (cli.py:198-203 protocol)
-    return {"value": len(c.dims) * sample_nnz / t, "unit": "nnz/s", "cores": threads, "kind": "port",
+    return {"value": len(c.dims) * sample_nnz / t, "unit": "nnz/s", "cores": threads, "kind": kind,
             "sample": f"{sample_nnz} nnz drawn from the {c.name} law (same dims, {laws_str(c)}, {c.value_dtype} values), "
-                      f"all {len(c.dims)} modes, Buffered mttkrp_par over {threads} partitions/threads, "
-                      f"mean of {reps} after 1 warm-up",
+                      f"all {len(c.dims)} modes, {what}, mean of {reps} after 1 warm-up",
             "seconds_per_step": t}
+
+
+def _load_installed_reference():
+    """The unmodified reference package installed into baseline/_ref (see
+    DESIGN.md §8), or None when that install is absent."""
+    ref_dir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "altotensor")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import altotensor
+
+    return altotensor
+
+
+def reference_step(cfg_id: int, sample: int, threads: int):
+    """One all-modes MTTKRP pass of the reference on a bounded same-law sample:
+    the installed unmodified reference when present, else the oracle port.
+    Returns (step, kind, description)."""
+    from paper_2102_10245_b200 import synth
+
+    st = synth.make_tensor(cfg_id, nnz=sample)
+    c = st.config
+    rng = np.random.default_rng(synth.SEED_FACTOR_BASE + cfg_id)
+    factors = [rng.random((d, c.rank)).astype(np.float32).astype(np.float64) for d in c.dims]
+    at = _load_installed_reference()
+    if at is not None:
+        # The reference's own public API and stock path, prepared as its CLI
+        # does (cli.py `_prepare`: partition, plan, flags outside the timed
+        # loop), then mttkrp_par per mode with every host thread.
+        tensor = at.build_alto(at.CooTensor(c.dims, st.coords, st.values.astype(np.float64)))
+        parts = at.partition(tensor, threads)
+        prepared = []
+        for mode in range(len(c.dims)):
+            plan = at.plan_conflicts(tensor, parts, mode)
+            t_m = at.apply_boundary_flags(tensor, plan) if (
+                plan.strategy is at.Strategy.ATOMIC and plan.flag_bit is not None) else tensor
+            prepared.append((t_m, plan))
+
+        def step():
+            for mode, (t_m, plan) in enumerate(prepared):
+                at.mttkrp_par(t_m, parts, plan, factors, mode, threads)
+
+        kind = "reference"
+        what = (f"unmodified reference altotensor {at.__version__} (baseline/_ref), mttkrp_par per mode "
+                f"with the auto conflict plan, {threads} partitions/workers")
+    else:
+        from oracle import alto_oracle as orc
+
+        lay = orc.build_layout(c.dims)
+        words, vals = orc.build(lay, st.coords, st.values.astype(np.float64))
+        offs, iv, _ = orc.partition(lay, words, threads)
+
+        def step():
+            for mode in range(len(c.dims)):
+                orc.mttkrp_buffered(lay, words, vals, factors, mode, offs, iv, workers=threads)
+
+        kind = "port"
+        what = f"oracle port of the reference mttkrp_par (Buffered, {threads} workers); baseline/_ref not installed"
+
+    return step, kind, what
 
 
 def run_reference(args):
@@ -131,21 +184,10 @@ def run_reference(args):
         return
     threads = len(os.sched_getaffinity(0))
     sample = args.cpu_sample
-    from oracle import alto_oracle as orc
+    step, kind, what = reference_step(args.config, sample, threads)
     from paper_2102_10245_b200 import synth
 
-    st = synth.make_tensor(args.config, nnz=sample)
-    c = st.config
-    lay = orc.build_layout(c.dims)
-    words, vals = orc.build(lay, st.coords, st.values.astype(np.float64))
-    rng = np.random.default_rng(synth.SEED_FACTOR_BASE + args.config)
-    factors = [rng.random((d, c.rank)).astype(np.float32).astype(np.float64) for d in c.dims]
-    offs, iv, _ = orc.partition(lay, words, threads)
-
-    def step():
-        for mode in range(len(c.dims)):
-            orc.mttkrp_buffered(lay, words, vals, factors, mode, offs, iv, workers=threads)
-
+    c = synth.CONFIGS[args.config]
     for _ in range(args.warmup):
         step()
     t0 = time.perf_counter()
@@ -160,9 +202,8 @@ def run_reference(args):
         "data": "synthetic (seeded, BASELINE.json law)",
         "config": {"workload": f"{c.name}: dims {list(c.dims)}, {laws_str(c)}, rank {c.rank}; CPU sample {sample} nnz",
                    "sample_nnz": sample, "threads": threads},
-        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} nnz of the {c.name} law, all modes, oracle port of the reference "
-                                   f"mttkrp_par (Buffered, {threads} workers)"},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": kind,
+                         "sample": f"{sample} nnz of the {c.name} law, all modes, {what}"},
         "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
