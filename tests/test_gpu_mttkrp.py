@@ -519,3 +519,44 @@ def test_fp32_accuracy_at_scale(at):
         assert float((fast - exact).norm() / exact.norm()) <= 1e-6
         del exact, fast
         torch.cuda.synchronize()
+
+
+def _installed_reference():
+    """The unmodified reference from baseline/_ref (bench.py's reference arm),
+    or None; this test is skipped where it was not installed."""
+    import importlib
+    import os
+    import sys
+
+    ref_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "altotensor")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    return importlib.import_module("altotensor")
+
+
+@pytest.mark.parametrize("cfg,nnz", [(1, 100_000), (2, 300_000), (4, 200_000)])
+def test_live_reference_bitwise(at, cfg, nnz):
+    """Device Buffered mttkrp_par == the installed reference's mttkrp_par,
+    bit for bit, on a same-law sample of a BASELINE config (reference
+    mttkrp.py:132-175, fixed partition count => deterministic)."""
+    ref = _installed_reference()
+    if ref is None:
+        pytest.skip("baseline/_ref not installed")
+    st = synth.make_tensor(cfg, nnz=nnz)
+    dims, rank = st.config.dims, st.config.rank
+    coords, values = st.coords, st.values.astype(np.float64)
+    factors = seeded_factors(dims, rank, seed=cfg)
+    r_alto = ref.build_alto(ref.CooTensor(dims, coords, values))
+    d_alto = at.build_alto(at.CooTensor(dims, coords, values))
+    assert np.array_equal(d_alto.indices, r_alto.indices)
+    assert np.array_equal(d_alto.values, r_alto.values)
+    for mode in range(len(dims)):
+        r_parts = ref.partition(r_alto, 16)
+        r_plan = ref.plan_conflicts(r_alto, r_parts, mode, force_strategy=ref.Strategy.BUFFERED)
+        want = ref.mttkrp_par(r_alto, r_parts, r_plan, factors, mode, 4)
+        d_parts = at.partition(d_alto, 16)
+        d_plan = at.plan_conflicts(d_alto, d_parts, mode, force_strategy=at.Strategy.BUFFERED)
+        got = at.mttkrp_par(d_alto, d_parts, d_plan, factors, mode, workers=4)
+        assert np.array_equal(got, want), (cfg, mode, rel_error(got, want))
