@@ -334,6 +334,66 @@ int alto_hot_plan(const int64_t* row_ptr, int64_t dim, int64_t tau, int32_t hmax
  * atomic path with several workers. */
 int alto_mttkrp(const alto_mttkrp_args* a, void* stream);
 
+/* Largest decoded coordinate of every mode (flag bits ignored), out_max
+ * (order,) device uint64.  Used to validate container files before a
+ * corrupt key can reach a kernel as an out-of-range row. */
+int alto_coord_max(const alto_layout* lay, const void* d_tables, const uint64_t* keys, int64_t m,
+                   uint64_t* out_max, void* stream);
+
+/* ---- K8/K9: slice interval buffers + deterministic pull ------------------
+ * The Buffered scheme of the reference (_par_buffered, mttkrp.py:132-175:
+ * per-partition interval buffers, then a pull in ascending partition order)
+ * and its Atomic scheme (_par_atomic, mttkrp.py:178-224: flagged elements
+ * merge with atomics, unflagged ones store directly) over the mode's
+ * row-major stream (alto_mode_stream with ALTO_MS_ROW_MAJOR, contiguous
+ * slices).  A slice (T/8 consecutive stream positions) is a partition whose
+ * output interval is contiguous: rows inside it are owned (plain stores),
+ * only its first/last row can be shared with a neighbouring slice (the
+ * boundary-flag rows of apply_boundary_flags, format.py:257-285).
+ *   atomic = 0 (Buffered): shared-row partials go to the slice's record
+ *     slots (slice_rec: per slice (first-run slot, last-run slot), -1 =
+ *     owned), then the pull sums each shared row's records in float64 in
+ *     slot order with a fixed two-level shape (chunks of 64 records:
+ *     chunk_off/chunk_seg/seg_chunk_off; multi-chunk segments `mseg` sum their
+ *     float64 chunk partials `part`): bitwise reproducible.
+ *   atomic = 1: shared rows (seg_row) are zeroed, then merged with RED.
+ * Empty rows are zero-filled by the stage (no memset).  Orders 3-5, ranks
+ * 16/32 (8/64: float32, Buffered), value/factor/out dtypes f32/f32/f32,
+ * f32/f32/f64, f64/f64/f64, f32/f64/f64 (float32 values, float64 factors:
+ * computed in float64).  Returns ALTO_EUNSUPPORTED for other shapes. */
+typedef struct alto_pull_args {
+  const alto_layout* lay;
+  const uint64_t* mkeys;        /* mode stream keys (alto_mode_stream)       */
+  const void* mvals;            /* mode stream values                        */
+  int32_t value_dtype;
+  int32_t tile;                 /* stream tile T (slices of T/8)             */
+  int64_t m;
+  int32_t mode;
+  int32_t rank;
+  int32_t factor_dtype;
+  int32_t out_dtype;
+  int32_t atomic;
+  int32_t pad_;
+  const void* factors[ALTO_MAX_ORDER];
+  void* out;                    /* (I_mode, rank), fully written             */
+  const int32_t* slice_rec;     /* (nslices, 2)                              */
+  void* rec;                    /* (n_rec, rank) in the factor dtype         */
+  int64_t n_seg;                /* shared rows                               */
+  const int32_t* seg_row;       /* (n_seg,)                                  */
+  int64_t n_chunks;
+  const int64_t* chunk_off;     /* (n_chunks+1,) record offsets              */
+  const int32_t* chunk_seg;     /* (n_chunks,)                               */
+  const int64_t* seg_chunk_off; /* (n_seg+1,)                                */
+  int64_t n_mseg;
+  const int32_t* mseg;          /* (n_mseg,) segments with > 1 chunk         */
+  double* part;                 /* (n_chunks, rank) float64 chunk partials   */
+} alto_pull_args;
+int alto_mttkrp_pull(const alto_pull_args* a, void* stream);
+/* Plan helper: first and last output row of every slice of a mode stream,
+ * first_last (nslices, 2) int32. */
+int alto_pull_slice_rows(const alto_layout* lay, const uint64_t* mkeys, int64_t m, int32_t mode, int32_t tile,
+                         int32_t* first_last, void* stream);
+
 /* Exact-order engine (deterministic; bitwise equal to the reference for
  * float64 data): for mode `mode`, `row_perm` lists element indices sorted by
  * (mode coordinate, element index) and `row_ptr` (I_mode+1) delimits rows.

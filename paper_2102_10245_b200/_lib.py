@@ -74,6 +74,37 @@ class CMttkrpArgs(Structure):
     ]
 
 
+class CPullArgs(Structure):
+    """alto_pull_args (include/alto_b200.h): K8/K9 slice buffers + pull."""
+    _fields_ = [
+        ("lay", POINTER(CLayout)),
+        ("mkeys", c_void_p),
+        ("mvals", c_void_p),
+        ("value_dtype", c_int32),
+        ("tile", c_int32),
+        ("m", c_int64),
+        ("mode", c_int32),
+        ("rank", c_int32),
+        ("factor_dtype", c_int32),
+        ("out_dtype", c_int32),
+        ("atomic", c_int32),
+        ("pad_", c_int32),
+        ("factors", c_void_p * ALTO_MAX_ORDER),
+        ("out", c_void_p),
+        ("slice_rec", c_void_p),
+        ("rec", c_void_p),
+        ("n_seg", c_int64),
+        ("seg_row", c_void_p),
+        ("n_chunks", c_int64),
+        ("chunk_off", c_void_p),
+        ("chunk_seg", c_void_p),
+        ("seg_chunk_off", c_void_p),
+        ("n_mseg", c_int64),
+        ("mseg", c_void_p),
+        ("part", c_void_p),
+    ]
+
+
 # (name, restype, argtypes) for every symbol of include/alto_b200.h
 SIGNATURES = [
     ("alto_last_error", c_char_p, []),
@@ -118,6 +149,9 @@ SIGNATURES = [
     ("alto_row_index_workspace_bytes", c_size_t, [c_int64, c_int64]),
     ("alto_row_index", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                  c_void_p, c_size_t, c_void_p]),
+    ("alto_coord_max", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    ("alto_mttkrp_pull", c_int32, [POINTER(CPullArgs), c_void_p]),
+    ("alto_pull_slice_rows", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     ("alto_mttkrp_exact", c_int32, [POINTER(CMttkrpArgs), c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     ("alto_mttkrp_coo", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, POINTER(c_void_p),
                                   c_void_p, c_int64, c_void_p]),

@@ -113,7 +113,26 @@ def deserialize(data: bytes, dtype=None) -> AltoTensor:
     off += nnz * nw * 8
     vals = np.frombuffer(data, dtype="<f8", count=nnz, offset=off)
     t = AltoTensor(layout, idx.astype(np.uint64), vals.astype(np.float64))
+    _check_coords(t)
     return _narrow(t, dtype)
+
+
+def _check_coords(t: AltoTensor) -> None:
+    """Every decoded coordinate must be below its mode extent: the masks
+    admit values up to 2^b_n - 1, and a corrupt or crafted file must fail
+    here (ContainerError) rather than drive out-of-range rows in a kernel."""
+    if t.nnz == 0:
+        return
+    torch = _torch()
+    from .layout import c_layout, device_tables
+
+    lay = t.layout
+    mx = torch.empty(lay.order, dtype=torch.int64, device=t.keys.device)
+    _lib.check(_lib.load().alto_coord_max(c_layout(lay), device_tables(lay).data_ptr(), t.keys.data_ptr(), t.nnz,
+                                          mx.data_ptr(), _lib.stream_ptr()), "alto_coord_max")
+    for n, (c, d) in enumerate(zip(mx.cpu().tolist(), lay.dims)):
+        if c >= d:
+            raise ContainerError(f"coordinate {c} of mode {n} out of range for extent {d}")
 
 
 def _narrow(t: AltoTensor, dtype) -> AltoTensor:
@@ -207,4 +226,6 @@ def read_alto(path: str, dtype=None) -> AltoTensor:
             pump(keys.view(torch.uint8).view(-1))
             pump(vals.view(torch.uint8).view(-1))
             torch.cuda.current_stream(dev).synchronize()
-    return _narrow(AltoTensor(layout, keys, vals), dtype)
+    t = AltoTensor(layout, keys, vals)
+    _check_coords(t)
+    return _narrow(t, dtype)

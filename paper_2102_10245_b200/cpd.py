@@ -236,7 +236,11 @@ class DeviceBackend:
             return mttkrp_stream(self.tensor, fdev, mode, out=out)
         if eng == "coo":
             return _coo_run(self.tensor, fdev, mode)
-        return mttkrp_deterministic(self.tensor, fdev, mode, self.offsets[mode], out=out)
+        od = None
+        if (allow_f32 and out is None and self.tensor.vals.dtype == torch.float32
+                and fdev[0].dtype == torch.float32):
+            od = torch.float32  # the pull engine may hand its float32 rows straight to the update
+        return mttkrp_deterministic(self.tensor, fdev, mode, self.offsets[mode], out=out, out_dtype=od)
 
 
 def _coo_run(tensor: AltoTensor, fdev: list, mode: int):

@@ -117,11 +117,65 @@ __global__ void delinearize_kernel(const __grid_constant__ DevLayout L, const ui
   }
 }
 
+// Per-mode maximum coordinate (container validation: a corrupt file must not
+// drive out-of-range factor/output rows).  Warp max, then one atomicMax per
+// warp and mode.
+template <int W>
+__global__ void coord_max_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ tab,
+                                 const uint64_t* __restrict__ keys, long long m,
+                                 unsigned long long* __restrict__ out) {
+  extern __shared__ uint64_t s_dec[];
+  copy_to_smem(s_dec, tab + static_cast<long long>(L.dec_off) * W, L.dec_bytes * 256 * W);
+  __syncthreads();
+  unsigned long long mx[ALTO_MAX_ORDER];
+  for (int n = 0; n < ALTO_MAX_ORDER; ++n) mx[n] = 0ull;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m; i += stride) {
+    const Key<W> p = decode_packed<W>(s_dec, L.dec_bytes, load_key<W>(keys, i));
+    for (int n = 0; n < L.order; ++n) {
+      const unsigned long long c = static_cast<unsigned long long>(packed_field<W>(p, L.pack_off[n], L.bits[n]));
+      mx[n] = c > mx[n] ? c : mx[n];
+    }
+  }
+  for (int n = 0; n < L.order; ++n) {
+    unsigned long long v = mx[n];
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long u = __shfl_down_sync(0xffffffffu, v, o);
+      v = u > v ? u : v;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out + n, v);
+  }
+}
+
 }  // namespace alto
 
 using namespace alto;
 
 extern "C" {
+
+int alto_coord_max(const alto_layout* lay, const void* d_tables, const uint64_t* keys, int64_t m,
+                   uint64_t* out_max, void* stream) {
+  int st = check_layout(lay);
+  if (st != ALTO_OK) return st;
+  cudaStream_t s = as_stream(stream);
+  ALTO_CUDA_TRY(cudaMemsetAsync(out_max, 0, sizeof(uint64_t) * lay->order, s));
+  if (m <= 0) return ALTO_OK;
+  const DevLayout d = make_dev_layout(lay);
+  const int block = 256;
+  const int grid = grid_for(m, block, kSMs * 4);
+  const size_t smem = static_cast<size_t>(d.dec_bytes) * 256 * d.n_words * sizeof(uint64_t);
+  const auto* tab = static_cast<const uint64_t*>(d_tables);
+  auto* o = reinterpret_cast<unsigned long long*>(out_max);
+  if (d.n_words == 1) {
+    ALTO_CUDA_TRY(cudaFuncSetAttribute(coord_max_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    coord_max_kernel<1><<<grid, block, smem, s>>>(d, tab, keys, m, o);
+  } else {
+    ALTO_CUDA_TRY(cudaFuncSetAttribute(coord_max_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    coord_max_kernel<2><<<grid, block, smem, s>>>(d, tab, keys, m, o);
+  }
+  ALTO_LAUNCH_CHECK("alto_coord_max");
+  return ALTO_OK;
+}
 
 const char* alto_last_error(void) { return g_err.c_str(); }
 int alto_version(void) { return 1; }

@@ -1,16 +1,27 @@
 """MTTKRP on the B200: drop-in for pkg/src/altotensor/mttkrp.py.
 
 Engines (all device code in libalto_b200.so):
-  * streaming tile kernel (`mttkrp_stream`, alto_mttkrp) — the fast path:
-    per-CTA interval buffers in shared memory with a float64 merge, or
-    float64 atomics for wide tiles.  Used for Atomic plans (like the
-    reference's atomic path it is not bitwise reproducible across runs).
-  * exact-order engine (`mttkrp_exact`, alto_mttkrp_exact) — deterministic:
-    per-row sums in element order, split at partition boundaries and merged
-    in ascending partition order, in float64.  This is exactly the
-    arithmetic order of mttkrp_seq (mttkrp.py:108-117) and of the Buffered
-    stage + pull (mttkrp.py:148-172), so results are bitwise equal to the
-    reference on float64 inputs and independent of `workers`.
+  * K8/K9 pull engine (`mttkrp_pull`, alto_mttkrp_pull, csrc/alto_pull.cuh)
+    over the mode's row-major stream: slice interval buffers + a fixed-order
+    float64 pull reduction — the reference's Buffered scheme
+    (mttkrp.py:132-175), bitwise reproducible and independent of
+    workers/partitions; with atomic=True its Atomic scheme (mttkrp.py:178-224:
+    rows shared between slices merge with atomics, owned rows are stored).
+    Buffered plans of large tensors and Atomic plans run here.
+  * exact-order engine (`mttkrp_exact`, alto_mttkrp_exact) — per-row sums in
+    element order, split at partition boundaries and merged in ascending
+    partition order, in float64: exactly the arithmetic order of mttkrp_seq
+    (mttkrp.py:108-117) and of the Buffered stage + pull (mttkrp.py:148-172),
+    so results are bitwise equal to the reference on float64 inputs.  Used
+    for Buffered plans of tensors up to EXACT_MAX_NNZ elements with rows of
+    at most EXACT_MAX_RUN elements.
+  * mode-stream kernel (`mttkrp_stream`, alto_mttkrp, csrc/alto_mstream.cuh)
+    — the fastest float32 path (round-robin lane groups, RED merges,
+    replicated hot rows); not bitwise reproducible (float atomics).  The
+    bench's device-timed step and the `atomic` CP-ALS backend.
+  * fixed-point streaming (`mttkrp_det`): int64 merges, deterministic; only a
+    fallback for shapes the pull engine does not cover.  Its scale comes
+    from a global bound, so rows of small magnitude keep fewer digits.
   * COO kernel (`mttkrp_oracle`) over a coordinate list.
 """
 
@@ -81,15 +92,24 @@ def _copy_stream(dev):
     return st
 
 
+# Pinned host factors are uploaded on a side stream.  By default the side
+# stream first waits for the current stream, so work the caller queued
+# before the call (e.g. a non_blocking device->host copy filling the pinned
+# factor) completes before the upload reads it.  OVERLAP_UPLOADS = True drops
+# that wait so an upload overlaps the previous call's kernels (bench.py's
+# end-to-end leg opts in: its pinned inputs are written once, up front).
+OVERLAP_UPLOADS = False
+
+
 def factors_to_device(factors, dtype=None, skip: int | None = None) -> list:
     """Factors as contiguous device tensors (float64 unless dtype/torch input
     says otherwise).  `skip`: a host factor the MTTKRP of that mode never
     reads (the output mode's) is not copied; a 1-row placeholder of the same
     dtype and rank stands in for it.  Pinned host torch tensors are copied
-    asynchronously on a side stream that the current stream then waits for,
-    so a caller's next upload overlaps the previous call's kernels (as with
-    any non_blocking copy, a pinned input must not be modified until the
-    stream is synchronized)."""
+    asynchronously on a side stream that the current stream then waits for
+    (the side stream waits for the current stream first unless
+    OVERLAP_UPLOADS is set; as with any non_blocking copy, a pinned input
+    must not be modified until the stream is synchronized)."""
     torch = _torch()
     dev = _lib.cuda_device()
     out = []
@@ -100,6 +120,8 @@ def factors_to_device(factors, dtype=None, skip: int | None = None) -> list:
             if cur is None:
                 cur = torch.cuda.current_stream(dev)
                 side = _copy_stream(dev)
+                if not OVERLAP_UPLOADS:
+                    side.wait_stream(cur)  # pending writes to the pinned inputs land first
             with torch.cuda.stream(side):
                 d = torch.empty(f.shape, dtype=f.dtype, device=dev)  # side-stream memory pool
                 d.copy_(f, non_blocking=True)
@@ -519,6 +541,186 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
     return out
 
 
+# ---- K8/K9: slice interval buffers + deterministic pull (alto_pull.cuh) ----
+# Records per level-1 pull chunk (kPullChunk in csrc/alto_pull.cuh).
+PULL_CHUNK = 64
+ALTO_MS_ROW_MAJOR = 1
+
+
+def pull_stream(tensor: AltoTensor, mode: int):
+    """The mode's row-major stream with contiguous slices (alto_mode_stream,
+    ALTO_MS_ROW_MAJOR): the ALTO elements stably sorted by the output
+    coordinate, ALTO order kept inside a row, cached per (mode, tile) like the
+    reference's per-mode plans (_make_backend, cpd.py:149-181).
+    -> (keys, values, tile) or None when the field layout does not fit."""
+    torch = _torch()
+    T = ms_tile(tensor)
+    key = ("pstream", mode, T)
+    hit = tensor._cache.get(key)
+    if hit is None:
+        lib = _lib.load()
+        lay = tensor.layout
+        m = tensor.nnz
+        dev = tensor.keys.device
+        vals = tensor.vals
+        ntiles = (m + T - 1) // T
+        skeys = torch.empty((max(ntiles * T, 1), lay.n_words), dtype=tensor.keys.dtype, device=dev)
+        svals = torch.empty(max(ntiles * T, 1), dtype=vals.dtype, device=dev)
+        wsb = int(lib.alto_mode_stream_workspace_bytes(m))
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals), m,
+                                  mode, T, ALTO_MS_ROW_MAJOR, None, skeys.data_ptr(), svals.data_ptr(),
+                                  ws.data_ptr(), wsb, _lib.stream_ptr())
+        del ws
+        if rc == _lib.ALTO_EUNSUPPORTED:
+            hit = False
+        else:
+            _lib.check(rc, "alto_mode_stream")
+            hit = (skeys, svals, T)
+        tensor._cache[key] = hit
+    return hit or None
+
+
+def pull_plan(tensor: AltoTensor, mode: int):
+    """Shared-row plan of the pull engine for one mode, cached.
+
+    A slice (T/8 consecutive positions of the row-major stream) owns every row
+    strictly inside its output interval; its first / last row is shared when
+    the neighbouring slice ends / starts with the same row (the rows
+    apply_boundary_flags would flag, format.py:257-285).  Each shared run gets
+    a record slot; a shared row's records are consecutive slots (element
+    order), summed by the pull in chunks of PULL_CHUNK records and then over
+    chunks.  Built on the device from the slices' first/last rows
+    (alto_pull_slice_rows)."""
+    torch = _torch()
+    ps = pull_stream(tensor, mode)
+    T = ps[2]
+    key = ("pplan", mode, T)
+    hit = tensor._cache.get(key)
+    if hit is not None:
+        return hit
+    m = tensor.nnz
+    dev = tensor.keys.device
+    ch = T // 8
+    ns = (m + ch - 1) // ch
+    fl = torch.empty((max(ns, 1), 2), dtype=torch.int32, device=dev)
+    _lib.check(_lib.load().alto_pull_slice_rows(c_layout(tensor.layout), ps[0].data_ptr(), m, mode, T,
+                                                fl.data_ptr(), _lib.stream_ptr()), "alto_pull_slice_rows")
+    first, last = fl[:ns, 0].long(), fl[:ns, 1].long()
+    sf = torch.zeros(ns, dtype=torch.bool, device=dev)
+    sl = torch.zeros(ns, dtype=torch.bool, device=dev)
+    if ns > 1:
+        sf[1:] = first[1:] == last[:-1]
+        sl[:-1] = last[:-1] == first[1:]
+    single = first == last
+    cnt = torch.where(single, (sf | sl).long(), sf.long() + sl.long())
+    start = torch.cumsum(cnt, 0) - cnt
+    slot_x = torch.where(sf, start, torch.full_like(start, -1))
+    slot_y = torch.where(sl, torch.where(single, start, start + sf.long()), torch.full_like(start, -1))
+    slice_rec = torch.stack([slot_x, slot_y], 1).to(torch.int32).contiguous()
+    n_rec = int(cnt.sum().item()) if ns else 0
+    rec_row = torch.empty(max(n_rec, 1), dtype=torch.long, device=dev)
+    rec_row[slot_x[sf]] = first[sf]
+    rec_row[slot_y[sl]] = last[sl]
+    rec_row = rec_row[:n_rec]
+    if n_rec:
+        change = torch.ones(n_rec, dtype=torch.bool, device=dev)
+        change[1:] = rec_row[1:] != rec_row[:-1]
+        seg_start = torch.nonzero(change).flatten()
+        seg_row = rec_row[seg_start].to(torch.int32).contiguous()
+        seg_off = torch.cat([seg_start, torch.tensor([n_rec], device=dev)])
+        counts = seg_off[1:] - seg_off[:-1]
+        nch = (counts + PULL_CHUNK - 1) // PULL_CHUNK
+        seg_chunk_off = torch.cat([torch.zeros(1, dtype=torch.long, device=dev), torch.cumsum(nch, 0)])
+        n_chunks = int(seg_chunk_off[-1].item())
+        chunk_seg = torch.repeat_interleave(torch.arange(seg_row.numel(), device=dev), nch)
+        j = torch.arange(n_chunks, device=dev) - seg_chunk_off[chunk_seg]
+        chunk_off = torch.cat([seg_off[chunk_seg] + j * PULL_CHUNK, torch.tensor([n_rec], device=dev)]).contiguous()
+        mseg = torch.nonzero(nch > 1).flatten().to(torch.int32).contiguous()
+        chunk_seg = chunk_seg.to(torch.int32).contiguous()
+    else:
+        seg_row = torch.zeros(1, dtype=torch.int32, device=dev)
+        seg_chunk_off = torch.zeros(1, dtype=torch.long, device=dev)
+        chunk_off = torch.zeros(1, dtype=torch.long, device=dev)
+        chunk_seg = torch.zeros(1, dtype=torch.int32, device=dev)
+        mseg = torch.zeros(0, dtype=torch.int32, device=dev)
+        n_chunks = 0
+    hit = {"slice_rec": slice_rec, "n_rec": n_rec, "seg_row": seg_row, "n_seg": int(seg_row.numel()) if n_rec else 0,
+           "chunk_off": chunk_off, "chunk_seg": chunk_seg, "seg_chunk_off": seg_chunk_off, "n_chunks": n_chunks,
+           "mseg": mseg, "n_mseg": int(mseg.numel())}
+    tensor._cache[key] = hit
+    return hit
+
+
+def pull_supported(tensor: AltoTensor, rank: int, fbytes: int, out_bytes: int = 8, atomic: bool = False) -> bool:
+    """Shapes the pull engine covers (else the caller uses another engine)."""
+    lay = tensor.layout
+    if not (tensor.nnz > 0 and 3 <= lay.order <= 5 and max(lay.bits) <= 31 and tensor.nnz < (1 << 32) - 1):
+        return False
+    f32_only = fbytes == 4 and out_bytes == 4 and not atomic and tensor.vals.element_size() == 4
+    return rank in (16, 32) or (rank in (8, 64) and f32_only)
+
+
+def mttkrp_pull(tensor: AltoTensor, fdev: list, mode: int, out=None, out_dtype=None, atomic: bool = False):
+    """K8/K9 MTTKRP -> (I_mode, R) device tensor (float64 unless out/out_dtype
+    says float32; float32 needs float32 values and factors).
+
+    atomic=False (Buffered): owned rows stored, shared rows pulled in a
+    fixed order -> bitwise reproducible.  atomic=True: shared rows merged
+    with RED (the Atomic scheme).  float32 values with float64 factors are
+    computed in float64 (the reference's arithmetic on upcast inputs).
+    Returns None when the shape is not covered (the caller falls back)."""
+    torch = _torch()
+    rank = int(fdev[0].shape[1])
+    dim = tensor.layout.dims[mode]
+    vals = tensor.vals
+    if vals.dtype == torch.float64 and fdev[0].dtype == torch.float32:
+        fdev = [f.double() for f in fdev]  # exact upcast
+    fb = fdev[0].element_size()
+    if out is None:
+        out = torch.empty((dim, rank), dtype=out_dtype or torch.float64, device=tensor.keys.device)
+    if out.dtype == torch.float32 and (fb != 4 or vals.dtype != torch.float32):
+        return None
+    if not pull_supported(tensor, rank, fb, out.element_size(), atomic):
+        return None
+    ps = pull_stream(tensor, mode)
+    if ps is None:
+        return None
+    plan = pull_plan(tensor, mode)
+    lay = tensor.layout
+    a = _lib.CPullArgs()
+    cl = c_layout(lay)
+    a.lay = ctypes.pointer(cl)
+    a.mkeys, a.mvals, a.value_dtype, a.tile = ps[0].data_ptr(), ps[1].data_ptr(), _dt_code(vals), ps[2]
+    a.m, a.mode, a.rank = tensor.nnz, mode, rank
+    fdt = {_dt_code(f) for f in fdev}
+    if len(fdt) != 1:
+        raise ValueError("factor matrices must share one dtype")
+    a.factor_dtype = fdt.pop()
+    a.out_dtype = _dt_code(out)
+    a.atomic = 1 if atomic else 0
+    for n, f in enumerate(fdev):
+        a.factors[n] = f.data_ptr()
+    a.out = out.data_ptr()
+    a.slice_rec = plan["slice_rec"].data_ptr()
+    rec = part = None
+    if not atomic and plan["n_rec"]:
+        rec = torch.empty((plan["n_rec"], rank), dtype=fdev[0].dtype, device=out.device)
+        part = torch.empty((max(plan["n_chunks"], 1), rank), dtype=torch.float64, device=out.device)
+    a.rec = None if rec is None else rec.data_ptr()
+    a.part = None if part is None else part.data_ptr()
+    a.n_seg, a.seg_row = plan["n_seg"], plan["seg_row"].data_ptr()
+    a.n_chunks = plan["n_chunks"] if not atomic else 0
+    a.chunk_off, a.chunk_seg = plan["chunk_off"].data_ptr(), plan["chunk_seg"].data_ptr()
+    a.seg_chunk_off = plan["seg_chunk_off"].data_ptr()
+    a.n_mseg, a.mseg = plan["n_mseg"], plan["mseg"].data_ptr() if plan["n_mseg"] else None
+    rc = _lib.load().alto_mttkrp_pull(ctypes.byref(a), _lib.stream_ptr())
+    if rc == _lib.ALTO_EUNSUPPORTED:
+        return None
+    _lib.check(rc, "alto_mttkrp_pull")
+    return out
+
+
 def row_index(tensor: AltoTensor, mode: int):
     """Per-mode (row_perm, row_ptr): elements sorted by (coordinate, position), cached."""
     torch = _torch()
@@ -626,12 +828,29 @@ def mttkrp_det(tensor: AltoTensor, fdev: list, mode: int, out=None):
     return out
 
 
-def mttkrp_deterministic(tensor: AltoTensor, fdev: list, mode: int, part_offsets=None, out=None):
-    """Deterministic MTTKRP: the exact-order engine (bitwise equal to the
-    reference) when the longest row is short, else the fixed-point streaming
-    kernel (bitwise reproducible, ~1e-13 relative to the exact sums)."""
-    if tensor.nnz > 0 and det_supported(tensor, fdev) and max_row_length(tensor, mode) > EXACT_MAX_RUN:
-        return mttkrp_det(tensor, fdev, mode, out=out)
+# Buffered plans up to this many elements (with rows no longer than
+# EXACT_MAX_RUN) run the exact-order engine, bitwise equal to the reference;
+# larger tensors run the K8/K9 pull engine (bitwise reproducible, ~1e-16
+# relative to the exact sums in float64).
+EXACT_MAX_NNZ = int(__import__("os").environ.get("ALTO_EXACT_MAX_NNZ", 4_000_000))
+
+
+def mttkrp_deterministic(tensor: AltoTensor, fdev: list, mode: int, part_offsets=None, out=None, out_dtype=None):
+    """Deterministic MTTKRP (the Buffered scheme, mttkrp.py:132-175).
+
+    * small tensors with short rows: the exact-order engine (bitwise equal
+      to the reference's Buffered / seq results on float64 data);
+    * otherwise the K8/K9 pull engine (slice interval buffers + fixed-order
+      float64 pull: bitwise reproducible, independent of workers/partitions);
+    * shapes the pull engine does not cover: the fixed-point streaming kernel
+      for long rows, else the exact-order engine."""
+    big = tensor.nnz > EXACT_MAX_NNZ
+    if tensor.nnz > 0 and (big or max_row_length(tensor, mode) > EXACT_MAX_RUN):
+        r = mttkrp_pull(tensor, fdev, mode, out=out, out_dtype=out_dtype)
+        if r is not None:
+            return r
+        if det_supported(tensor, fdev) and max_row_length(tensor, mode) > EXACT_MAX_RUN:
+            return mttkrp_det(tensor, fdev, mode, out=out)
     return mttkrp_exact(tensor, fdev, mode, part_offsets, out=out)
 
 
@@ -704,9 +923,11 @@ def mttkrp_par(tensor: AltoTensor, parts: PartitionSet, plan: ConflictPlan, fact
                workers: int = 1):
     """Plan-driven MTTKRP (mttkrp.py:227-251).
 
-    Buffered plans run the exact-order engine over the plan's partitions
-    (bitwise deterministic, independent of `workers`); Atomic plans run the
-    streaming kernel.  `workers` is validated but has no effect on device.
+    Buffered plans run the deterministic engines (exact-order engine over the
+    plan's partitions for small tensors, else the K8/K9 pull engine; bitwise
+    reproducible, independent of `workers`); Atomic plans run the pull
+    engine's atomic scheme.  `workers` is validated but has no effect on
+    device.
     """
     _check_factors(tensor.layout.dims, factors, mode)
     if workers < 1:
@@ -722,7 +943,11 @@ def mttkrp_par(tensor: AltoTensor, parts: PartitionSet, plan: ConflictPlan, fact
     if plan.flag_bit is not None and plan.overlaps is not None and any(plan.overlaps) and tensor.nnz:
         if not _any_flag(tensor, plan.flag_bit):
             raise ValueError("plan expects boundary flags; apply_boundary_flags first")
-    return _finish(mttkrp_stream(tensor, fdev, mode), like)
+    # Atomic scheme: rows shared between slices merge with atomics, owned
+    # rows are stored directly (the pull engine's boundary flags); the
+    # streaming kernel for shapes it does not cover
+    out = mttkrp_pull(tensor, fdev, mode, atomic=True)
+    return _finish(out if out is not None else mttkrp_stream(tensor, fdev, mode), like)
 
 
 def mttkrp(tensor: AltoTensor, factors, mode: int, workers: int = 1, partitions: int | None = None,

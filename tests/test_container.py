@@ -116,3 +116,25 @@ class TestValidation:
 
     def test_is_value_error(self, at):
         assert issubclass(at.ContainerError, ValueError)
+
+
+@pytest.mark.gpu
+def test_out_of_range_coordinate_rejected(at, tmp_path):
+    """A key whose decoded coordinate is >= the mode extent (the masks admit
+    up to 2^b_n - 1) raises ContainerError on read, before any kernel can
+    use it as a row (advisor finding: corrupt .alto files)."""
+    coo = at.CooTensor((5, 3, 7), np.array([[4, 2, 6], [0, 0, 0]]), np.array([1.0, 2.0]))
+    blob = bytearray(at.serialize(at.build_alto(coo)))
+    lay = at.build_masks((5, 3, 7))
+    bad = at.linearize(lay, (4, 2, 6)) | lay.masks[0]  # mode-0 coordinate 7 >= 5
+    nnz, nw = 2, 1
+    off = len(blob) - nnz * 8 - nnz * nw * 8
+    words = np.frombuffer(bytes(blob[off:off + nnz * 8]), dtype="<u8").copy()
+    words[np.argmax(words)] = bad
+    blob[off:off + nnz * 8] = words.astype("<u8").tobytes()
+    with pytest.raises(at.ContainerError, match="out of range"):
+        at.deserialize(bytes(blob))
+    p = tmp_path / "bad.alto"
+    p.write_bytes(bytes(blob))
+    with pytest.raises(at.ContainerError, match="out of range"):
+        at.read_alto(str(p))
