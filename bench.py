@@ -214,19 +214,20 @@ def laws_str(c) -> str:
     return "modes: " + ", ".join(f"zipf({s})" if law == "zipf" else "uniform" for law, s in c.laws)
 
 
-def traffic_from_profile(kernel_tag: str):
-    """Per-launch DRAM bytes (read + write) of the dominant kernel from the
-    latest committed `ncu --set full` capture of this workload (profiles/)."""
+def traffic_from_profile(cfg_id: int):
+    """Per-launch DRAM bytes (read + write) of the dominant kernel, averaged
+    over the captured launches of the latest committed `ncu --set full`
+    capture of this workload (profiles/r*_cfg<id>_mstream_ncu.json)."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_mstream_kernel_ncu.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_cfg{cfg_id}_mstream_ncu.json")))
     if not files:
         return None, None
     try:
         rows = json.load(open(files[-1]))
         vals = []
         for r in rows:
-            if kernel_tag in r["kernel"]:
+            if "mstream_kernel" in r["kernel"]:
                 rd = float(r["dram__bytes_read.sum"]["value"])
                 wr = float(r["dram__bytes_write.sum"]["value"])
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -241,7 +242,72 @@ def flush_l2(buf):
     buf.add_(1.0)
 
 
+def _events(n):
+    import torch
+
+    return [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+
+
+def cache_bytes(alto, keys) -> int:
+    """HBM bytes held by the tensor's cached plans whose cache key starts with one of `keys`."""
+    import torch
+
+    tot = 0
+
+    def walk(v):
+        nonlocal tot
+        if isinstance(v, torch.Tensor):
+            tot += v.numel() * v.element_size()
+        elif isinstance(v, (tuple, list)):
+            for x in v:
+                walk(x)
+        elif isinstance(v, dict):
+            for x in v.values():
+                walk(x)
+
+    for k, v in alto._cache.items():
+        name = k[0] if isinstance(k, tuple) else k
+        if name in keys:
+            walk(v)
+    return tot
+
+
+def time_modes(fn, N, steps, l2, stream):
+    """Per-mode CUDA-event times (ms) of fn(mode), L2 flushed before each
+    all-modes step; returns (step_ms list, per-mode mean ms)."""
+    import torch
+
+    step_ev = _events(steps)
+    mode_ev = [_events(N) for _ in range(steps)]
+    for k in range(steps):
+        flush_l2(l2)
+        step_ev[k][0].record(stream)
+        for n in range(N):
+            mode_ev[k][n][0].record(stream)
+            fn(n)
+            mode_ev[k][n][1].record(stream)
+        step_ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    mode_ms = [sum(mode_ev[k][n][0].elapsed_time(mode_ev[k][n][1]) for k in range(steps)) / steps for n in range(N)]
+    return step_ms, mode_ms
+
+
+def timed_once(fn, stream):
+    import torch
+
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b)
+
+
 def run_b200(args):
+    import importlib
+
     import torch
     import torch.distributed as dist
 
@@ -249,8 +315,8 @@ def run_b200(args):
     from paper_2102_10245_b200 import synth
     from paper_2102_10245_b200.format import AltoTensor, build_alto_device
     from paper_2102_10245_b200.layout import build_masks
-    from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
 
+    mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
     ws, rank, local = dist_env()
     # functional check of the multi-rank path on a one-GPU box only
     # (ALTO_BENCH_TEST_GLOO=1: every rank on cuda:0, gloo collectives; numbers
@@ -278,177 +344,243 @@ def run_b200(args):
     torch.cuda.synchronize()
     t_gen = time.time() - t_gen
     dims = cfg.dims
-    R = cfg.rank
+    R = args.rank or cfg.rank
+    N = len(dims)
     lay = build_masks(dims)
-    # ALTO build on device (whole tensor), then keep this rank's key-range shard
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    full = build_alto_device(lay, coords, vals)
-    e1.record()
-    torch.cuda.synchronize()
-    build_ms = e0.elapsed_time(e1)
-    del coords, vals
+    stream = torch.cuda.current_stream()
+    exch_bytes = 0
+    shard_info = None
     if ws > 1:
-        offs = at.format.partition_offsets(full.nnz, ws)
-        a, b = int(offs[rank]), int(offs[rank + 1])
-        alto = AltoTensor(lay, full.keys[a:b].clone(), full.vals[a:b].clone())
-        del full
+        from paper_2102_10245_b200.dist import build_shard
+
+        e0 = time.time()
+        alto, shard_info = build_shard(lay, coords, vals, rank, ws, R)
+        torch.cuda.synchronize()
+        build_ms = (time.time() - e0) * 1e3
     else:
-        alto = full
+        build_ms = timed_once(lambda: None, stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        alto = build_alto_device(lay, coords, vals)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        build_ms = e0.elapsed_time(e1)
+    del coords, vals
     M = alto.nnz
     fdt = np.float32 if cfg.value_dtype == "float32" else np.float64
     rng = np.random.default_rng(synth.SEED_FACTOR_BASE + args.config)
     factors_host = [rng.random((d, R)).astype(fdt) for d in dims]
-    fdev = factors_to_device(factors_host)
+    fdev = mk.factors_to_device(factors_host)
     if args.out is None:
         args.out = "f32" if vdt == torch.float32 else "f64"
     odt = torch.float32 if args.out == "f32" else torch.float64
     outs = [torch.empty((d, R), dtype=odt, device=dev) for d in dims]
     l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream()
-    N = len(dims)
+    kb, vb, fb = 8 * lay.n_words, 4 if vdt == torch.float32 else 8, np.dtype(fdt).itemsize
+    peak, peak_kind = measured_peaks()
     xplans = None
-    exch_bytes = 0
     if ws > 1:
         # shared-row exchange plan per mode (dist.py): only rows touched by
-        # >= 2 key-range shards cross NVLink, in one all-reduce per mode
-        from paper_2102_10245_b200.dist import DeviceOps, ShardRows, reduce_shared
+        # >= 2 key-range shards cross NVLink (owner-directed reduce + return)
+        from paper_2102_10245_b200.dist import DeviceOps, ShardRows, exchange_shared
 
         xops = DeviceOps(alto, R)
         xplans = [ShardRows(xops.touched_rows(n)) for n in range(N)]
         exch_bytes = sum(p.n_shared for p in xplans) * R * (4 if args.out == "f32" else 8)
 
-    def step(ev=None):
-        for mode in range(N):
-            if ev is not None:
-                ev[mode][0].record(stream)
-            mttkrp_stream(alto, fdev, mode, out=outs[mode], tile=args.tile, hot=not args.no_hot)
-            if ev is not None:
-                ev[mode][1].record(stream)
-            if ws > 1:
-                reduce_shared(outs[mode], xplans[mode], xops)
+    # ---- one-time per-mode plans (timed; excluded from the per-step time like
+    # the reference's partition/plan prep, cli.py:194) ---------------------
+    def plan_leg(build, keys):
+        for k in [k for k in alto._cache if (k[0] if isinstance(k, tuple) else k) in keys]:
+            del alto._cache[k]
+        torch.cuda.empty_cache()
+        ms = timed_once(build, stream)
+        return {"plan_build_ms": ms, "plan_bytes": cache_bytes(alto, keys)}
+
+    def build_ms_plans():
+        for n in range(N):
+            mk.mttkrp_stream(alto, fdev, n, out=outs[n], hot=not args.no_hot)
+
+    def build_pull_plans():
+        for n in range(N):
+            mk.pull_stream(alto, n)
+            mk.pull_plan(alto, n)
+
+    def build_alto_plans():
+        for n in range(N):
+            mk.packed_keys(alto)
+            mk.subtile_order(alto, n)
+
+    ms_keys = ("mstream", "hotms", "hotslots", "row_index", "packed")
+    plans = {"mode_stream": plan_leg(build_ms_plans, ms_keys)}
+
+    def step_stream(n):
+        mk.mttkrp_stream(alto, fdev, n, out=outs[n], hot=not args.no_hot)
+        if ws > 1:
+            exchange_shared(outs[n], xplans[n], xops)
 
     for _ in range(max(args.warmup, 3)):
-        step()
+        for n in range(N):
+            step_stream(n)
     torch.cuda.synchronize()
-    # timed region: per-step events (L2 flushed before each step, outside the events)
-    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-    mode_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(N)]
-               for _ in range(args.steps)]
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush_l2(l2)
-            step_ev[k][0].record(stream)
-            step(mode_ev[k])
-            step_ev[k][1].record(stream)
-        torch.cuda.synchronize()
+        step_ms, mode_ms = time_modes(step_stream, N, args.steps, l2, stream)
     if ws > 1:
         dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in step_ev]
     ms = sum(step_ms) / len(step_ms)
-    mode_ms = [sum(mode_ev[k][n][0].elapsed_time(mode_ev[k][n][1]) for k in range(args.steps)) / args.steps
-               for n in range(N)]
     t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms_max = float(t_ms.item())
     value = N * nnz_total / (ms_max * 1e-3)
 
-    # roofline of the dominant kernel (the streaming MTTKRP), per mode
-    peak, peak_kind = measured_peaks()
-    kb, vb, fb = 8 * lay.n_words, 4 if vdt == torch.float32 else 8, np.dtype(fdt).itemsize
     per_mode = []
     for n in range(N):
         ba = bytes_alg(dims, M, kb, vb, R, fb, n)
         per_mode.append({"mode": n, "kernel_ms": mode_ms[n], "bytes_alg": ba,
-                         "achieved_gbs": ba / (mode_ms[n] * 1e-3) / 1e9,
-                         "nnz_per_s": M / (mode_ms[n] * 1e-3)})
+                         "achieved_gbs": ba / (mode_ms[n] * 1e-3) / 1e9, "nnz_per_s": M / (mode_ms[n] * 1e-3)})
     tot_b = sum(p["bytes_alg"] for p in per_mode)
-    # our kernels per step: the streaming MTTKRP of each mode + its hot-row
-    # reduction when the mode has hot rows (the output zeroing is a memset)
-    mk = __import__("importlib").import_module("paper_2102_10245_b200.mttkrp")
+    achieved = tot_b / (sum(mode_ms) * 1e-3) / 1e9
     ms_used = all(alto._cache.get(("mstream", n, alto.vals.dtype, mk.ms_tile(alto), mk.MS_ORDER, mk.MS_RR))
                   for n in range(N))
-    kernel_name = ("alto::mstream_kernel (alto_mstream.cuh)" if ms_used
-                   else "alto::planned_kernel (alto_fast.cuh)")
+    kernel_name = "alto::mstream_kernel (alto_mstream.cuh)" if ms_used else "alto::planned_kernel (alto_fast.cuh)"
     launches_per_step = 0
     for n in range(N):
         launches_per_step += 1
         if ms_used and alto.vals.dtype == torch.float32:
-            launches_per_step += len(mk.ms_pairs(dims, n, R, 4))  # alto_krp_pair tables
+            launches_per_step += len(mk.ms_pairs(dims, n, R, 4))
         if not args.no_hot:
             hp = (alto._cache.get(("hotms", n, R, odt, mk.ms_tile(alto), mk.MS_ORDER)) if ms_used
                   else alto._cache.get(("hot", n, R, odt)))
             launches_per_step += 1 if hp else 0
-    tot_t = sum(mode_ms) * 1e-3
-    achieved = tot_b / tot_t / 1e9
     traffic, traffic_src = None, None
-    if ws == 1 and nnz_total == cfg.nnz and args.config == 2 and args.out == "f32" and not args.no_hot:
-        traffic, traffic_src = traffic_from_profile("mstream_kernel<1, float, float, 3, 16")
+    if ws == 1 and nnz_total == cfg.nnz and args.out == "f32" and not args.no_hot and R == cfg.rank:
+        traffic, traffic_src = traffic_from_profile(args.config)
+    for k in [k for k in alto._cache if (k[0] if isinstance(k, tuple) else k) in ("mstream", "hotms")]:
+        del alto._cache[k]
+    torch.cuda.empty_cache()
 
-    # end-to-end through the reference-facing API: mttkrp_par with an Atomic plan
-    # (the CLI protocol: prepare once, cli.py:194; per step host factors in,
-    # float64 result out, cli.py:198-203)
-    parts = at.partition(alto, 8)
-    plans, flagged = [], []
-    for n in range(N):
-        p = at.plan_conflicts(alto, parts, n, force_strategy=at.Strategy.ATOMIC)
-        plans.append(p)
-        flagged.append(at.apply_boundary_flags(alto, p) if p.flag_bit is not None else alto)
+    def path_line(name, fn, plan):
+        for _ in range(2):
+            for n in range(N):
+                fn(n)
+        _s, pm = time_modes(fn, N, max(3, args.steps // 2), l2, stream)
+        ba = [bytes_alg(dims, M, kb, vb, R, fb, n) for n in range(N)]
+        return dict(plan, kernel=name, per_mode_ms=pm, nnz_per_s=N * M / (sum(pm) * 1e-3),
+                    roofline_frac=sum(ba) / (sum(pm) * 1e-3) / 1e9 / peak)
+
+    paths = {}
+    if ws == 1 and not args.skip_paths:
+        # the paper's Buffered scheme: K8/K9 slice interval buffers + deterministic pull
+        # (the default `auto` API path for large tensors)
+        plans["pull"] = plan_leg(build_pull_plans, ("pstream", "pplan", "packed"))
+        if mk.mttkrp_pull(alto, fdev, 0, out=outs[0]) is not None:
+            paths["buffered_pull"] = path_line("alto::pull_stage_kernel + pull_chunk/seg (alto_pull.cuh), "
+                                               "Buffered, deterministic",
+                                               lambda n: mk.mttkrp_pull(alto, fdev, n, out=outs[n]), plans["pull"])
+            paths["atomic_pull"] = path_line("alto::pull_stage_kernel (alto_pull.cuh), Atomic scheme",
+                                             lambda n: mk.mttkrp_pull(alto, fdev, n, out=outs[n], atomic=True),
+                                             {})
+        for k in [k for k in alto._cache if (k[0] if isinstance(k, tuple) else k) in ("pstream",)]:
+            del alto._cache[k]
+        torch.cuda.empty_cache()
+        # the single mode-agnostic ALTO copy (packed keys + 1-byte sub-tile order per mode)
+        if R in (16, 32) and max(lay.bits) <= 31:
+            plans["alto_order"] = plan_leg(build_alto_plans, ("packed", "pos"))
+            paths["alto_order"] = path_line("alto::planned_kernel (alto_fast.cuh), ALTO order, single copy",
+                                            lambda n: mk.mttkrp_stream(alto, fdev, n, out=outs[n], planned="pos"),
+                                            plans["alto_order"])
+        paths["mode_stream"] = dict(plans["mode_stream"], kernel=kernel_name, per_mode_ms=mode_ms,
+                                    nnz_per_s=value, roofline_frac=achieved / peak)
+        for k in [k for k in alto._cache if (k[0] if isinstance(k, tuple) else k) in ("pos",)]:
+            del alto._cache[k]
+        torch.cuda.empty_cache()
+
+    # ---- end to end through the reference-facing API (cli.py:194-203
+    # protocol: prepare once; per step host factors in, float64 result out),
+    # with the default auto plan (Buffered on every mode -> pull engine) --
+    mk.OVERLAP_UPLOADS = True  # pinned inputs are written once, before the timed loop
+    parts = at.partition(alto, 16)
     fpin = [torch.from_numpy(f).pin_memory() for f in factors_host]
     opin = [torch.empty((d, R), dtype=torch.float64).pin_memory() for d in dims]
-
-    # each mode's result is read back on a copy stream, so mode n's
-    # device->host copy overlaps mode n+1's kernels (fresh output per call;
-    # record_stream keeps it alive until its copy has run)
     d2h_stream = torch.cuda.Stream(device=dev)
 
-    def e2e_step():
+    def e2e_leg(force):
+        pl, fl = [], []
         for n in range(N):
-            o = at.mttkrp_par(flagged[n], parts, plans[n], fpin, n, workers=1)
-            d2h_stream.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(d2h_stream):
-                opin[n].copy_(o, non_blocking=True)
-            o.record_stream(d2h_stream)
-        torch.cuda.synchronize()
+            p = at.plan_conflicts(alto, parts, n, force_strategy=force)
+            pl.append(p)
+            fl.append(at.apply_boundary_flags(alto, p) if (p.strategy is at.Strategy.ATOMIC
+                                                            and p.flag_bit is not None) else alto)
 
-    for _ in range(2):
-        e2e_step()
-    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ee0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    ee1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = ee0.elapsed_time(ee1) / args.steps
-    t_e = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t_e.item())
+        def e2e_step():
+            for n in range(N):
+                o = at.mttkrp_par(fl[n], parts, pl[n], fpin, n, workers=1)
+                d2h_stream.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(d2h_stream):
+                    opin[n].copy_(o, non_blocking=True)
+                o.record_stream(d2h_stream)
+            torch.cuda.synchronize()
+
+        for _ in range(2):
+            e2e_step()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) / args.e2e_steps
+        t_e = torch.tensor([t], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        return float(t_e.item()), [p.strategy.value for p in pl]
+
+    e2e_ms, e2e_strat = e2e_leg(None)
+    e2e_atomic_ms = None
+    if not args.skip_paths:
+        e2e_atomic_ms, _ = e2e_leg(at.Strategy.ATOMIC)
     h2d = sum(sum(d * R * fb for m, d in enumerate(dims) if m != n) for n in range(N))  # output factor not sent
     d2h = sum(d * R * 8 for d in dims)
+    for k in [k for k in alto._cache if (k[0] if isinstance(k, tuple) else k) in ("pstream",)]:
+        del alto._cache[k]
+    torch.cuda.empty_cache()
 
-    # CP-ALS iteration time (device loop, streaming backend), single GPU only
+    # ---- CP-ALS iteration time (device loop), single GPU only -------------
     cpals = None
     if ws == 1 and not args.skip_cpals:
         from paper_2102_10245_b200.cpd import DeviceCpAls
 
-        st_als = DeviceCpAls(alto, R, seed=0, backend="atomic", partitions=8)
-        st_als.sweep()
-        torch.cuda.synchronize()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c0.record(stream)
-        iters = 3
-        for _ in range(iters):
-            st_als.sweep()
-        c1.record(stream)
-        torch.cuda.synchronize()
-        cpals = c0.elapsed_time(c1) / iters
+        cpals = {}
+        iters = cfg.als_iters or 10
+        for backend in ("auto", "atomic"):
+            for k in list(alto._cache):
+                if (k[0] if isinstance(k, tuple) else k) not in ("packed",):
+                    del alto._cache[k]
+            torch.cuda.empty_cache()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st_als = DeviceCpAls(alto, R, seed=0, backend=backend, partitions=16)
+            m0 = st_als.mttkrp(0)
+            st_als.fit(m0, 0)
+            torch.cuda.synchronize()
+            setup_ms = (time.perf_counter() - t0) * 1e3
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            c0.record(stream)
+            for _ in range(iters):
+                st_als.sweep()
+            c1.record(stream)
+            torch.cuda.synchronize()
+            wall = (time.perf_counter() - t0) * 1e3
+            cpals[backend] = {"ms_per_iter": c0.elapsed_time(c1) / iters, "iters": iters,
+                              "setup_ms_incl_plans_and_initial_fit": setup_ms,
+                              f"total_ms_{iters}_iters_incl_setup": setup_ms + wall}
+            del st_als
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.skip_cpu:
@@ -463,28 +595,32 @@ def run_b200(args):
             "data": f"synthetic (seeded; BASELINE.json {cfg.name} law; generated on {args.gen})",
             "config": {"workload": f"{cfg.name}: {'x'.join(map(str, dims))}, {nnz_total} nnz, {laws_str(cfg)}, "
                                    f"{cfg.values} {cfg.value_dtype} values, rank {R}; step = MTTKRP all {N} modes",
-                       "nnz": nnz_total, "rank": R, "tile": args.tile, "key_bits": lay.total_bits,
-                       "out_dtype": args.out, "hot_plan": not args.no_hot,
+                       "nnz": nnz_total, "rank": R, "key_bits": lay.total_bits, "out_dtype": args.out,
+                       "hot_plan": not args.no_hot,
                        "l2": "flushed (256 MB write) before every timed step; keys+values "
                              f"{M * (kb + vb) / 1e6:.0f} MB > 126 MB L2",
                        "parallelism": f"key-range shards x{ws}" if ws > 1 else "1 GPU",
-                       "exchange_bytes_per_step": exch_bytes},
+                       "exchange_bytes_per_step": exch_bytes, "shards": shard_info},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "traffic": traffic, "traffic_source": traffic_src,
-                         "bytes_alg_per_launch": tot_b / N,
-                         "kernel": kernel_name,
+                         "bytes_alg_per_launch": tot_b / N, "kernel": kernel_name,
                          "timing": "per-mode CUDA events around the whole MTTKRP call (output zeroing, "
-                                   "streaming kernel, hot-row reduction)",
+                                   "mode-stream kernel, hot-row reduction)",
                          "per_mode": per_mode},
+            "paths": paths,
+            "plans": plans,
             "e2e": {"value": N * nnz_total / (e2e_ms * 1e-3), "unit": "nnz/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
-                    "api": "paper_2102_10245_b200.mttkrp_par (Atomic plan) with pinned host fp32 factors in, "
-                           "float64 result copied to pinned host memory on a copy stream (overlapping the next mode's kernels), every mode"},
+                    "d2h_bytes_per_step": d2h, "plan": e2e_strat,
+                    "api": "paper_2102_10245_b200.mttkrp_par with the default (auto) conflict plan over 16 "
+                           "partitions (Buffered on every mode -> K8/K9 pull engine), pinned host float32 factors "
+                           "in, float64 result copied to pinned host memory on a copy stream, every mode",
+                    "atomic_plan_value": (N * nnz_total / (e2e_atomic_ms * 1e-3)) if e2e_atomic_ms else None},
             "gpu_launches": args.steps * launches_per_step,
             "clocks": clk.summary(),
             "build_ms": build_ms, "gen_s": t_gen,
-            "cpals_ms_per_iter": cpals,
+            "cpals": cpals,
+            "cpals_ms_per_iter": cpals["auto"]["ms_per_iter"] if cpals else None,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -498,7 +634,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--rank", type=int, default=0, help="override the config's rank (rank sweep)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--skip-paths", action="store_true", help="only the headline mode-stream step")
     ap.add_argument("--nnz", type=int, default=0, help="override nnz (testing)")
     ap.add_argument("--tile", type=int, default=1024)
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)

@@ -482,6 +482,10 @@ int alto_pack_rows(const void* src, int32_t dtype, const int64_t* rows, int64_t 
                    void* stream);
 int alto_unpack_rows(void* dst, int32_t dtype, const int64_t* rows, int64_t n, int32_t rank, const void* buf,
                      void* stream);
+/* dst[rows[k]] += buf[k] (rows unique within a call): the owner-side reduce of
+ * the owner-directed shared-row exchange (dist.py). */
+int alto_add_rows(void* dst, int32_t dtype, const int64_t* rows, int64_t n, int32_t rank, const void* buf,
+                  void* stream);
 /* Cast helpers for factor uploads: out32[i] = (float)in64[i]. */
 int alto_cast_f64_f32(const double* in, float* out, int64_t n, void* stream);
 int alto_cast_f32_f64(const float* in, double* out, int64_t n, void* stream);

@@ -172,6 +172,7 @@ SIGNATURES = [
     ("alto_fixed_to_float", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p]),
     ("alto_pack_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_unpack_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    ("alto_add_rows", c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_gram_masked", c_int32, [c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t,
                                    c_void_p]),
     ("alto_solve_rows", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t,

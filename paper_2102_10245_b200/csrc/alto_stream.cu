@@ -288,7 +288,9 @@ __global__ void pack_rows_kernel(const T* __restrict__ src, const long long* __r
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total; i += stride) {
     const long long k = i / R;
     const long long g = rows[k] * R + (i - k * R);
-    if (unpack)
+    if (unpack == 2)
+      const_cast<T*>(src)[g] += dst[i];  // owner-side reduce of a received partial (rows unique per call)
+    else if (unpack)
       const_cast<T*>(src)[g] = dst[i];
     else
       dst[i] = src[g];
@@ -325,6 +327,22 @@ int alto_unpack_rows(void* dst, int32_t dtype, const int64_t* rows, int64_t n, i
     pack_rows_kernel<double><<<grid_for(n * rank, 256), 256, 0, s>>>(
         static_cast<const double*>(dst), r, n, rank, const_cast<double*>(static_cast<const double*>(buf)), 1);
   ALTO_LAUNCH_CHECK("alto_unpack_rows");
+  return ALTO_OK;
+}
+
+int alto_add_rows(void* dst, int32_t dtype, const int64_t* rows, int64_t n, int32_t rank, const void* buf,
+                  void* stream) {
+  if (n <= 0) return ALTO_OK;
+  cudaStream_t s = as_stream(stream);
+  const auto* r = reinterpret_cast<const long long*>(rows);
+  if (dtype == ALTO_F32)
+    pack_rows_kernel<float><<<grid_for(n * rank, 256), 256, 0, s>>>(static_cast<const float*>(dst), r, n, rank,
+                                                                     const_cast<float*>(static_cast<const float*>(buf)),
+                                                                     2);
+  else
+    pack_rows_kernel<double><<<grid_for(n * rank, 256), 256, 0, s>>>(
+        static_cast<const double*>(dst), r, n, rank, const_cast<double*>(static_cast<const double*>(buf)), 2);
+  ALTO_LAUNCH_CHECK("alto_add_rows");
   return ALTO_OK;
 }
 }  // extern "C"

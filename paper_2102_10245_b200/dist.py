@@ -6,18 +6,28 @@ paper lists distributed memory as future work).  Here each rank
 key range of the sorted ALTO stream — exactly an ALTO partition
 (format.py:127-154) — and full-size factor matrices.
 
+Shards (build_shard): every rank linearizes the coordinates it was handed
+(K1), picks the cut keys from a strided sample so that the shards balance a
+cost model — elements x (key + value bytes) plus, per mode, rows touched x
+R x factor bytes (each sampled element carries 1/count of its row, so a
+range's weight counts the rows it touches; Zipf tails make equal-nnz shards
+unequal in gather cost) — and then sorts only the elements of its own key
+range (K2).  The API-level `partition` stays equal-nnz.
+
 Per mode n:
   1. local MTTKRP over the shard (rows touched only by this shard are final);
-  2. shared-row reduction: rows touched by >= 2 shards are packed into one
-     compact buffer and summed with a single all-reduce (volume = shared
-     rows x R, not I_n x R);
-  3. every rank solves the rows it touches (X V = M); rows shared between
-     shards are solved redundantly by each toucher, so no factor rows need to
-     be sent back;
+  2. owner-directed shared-row exchange (exchange_shared): every row touched
+     by >= 2 shards has one owner (its lowest-rank toucher); the other
+     touchers send their partial rows to the owner in one grouped
+     send/recv (NCCL group: ncclSend/ncclRecv), the owner adds them in rank
+     order (deterministic) and sends the reduced rows back to exactly the
+     ranks that touch them — each rank moves only the shared rows it
+     touches, never a global all-reduce over I_n or over all shared rows;
+  3. every rank solves the rows it touches (X V = M); shared rows are
+     solved redundantly by each toucher, so no factor rows are sent back;
   4. column norms, the Gram of the new factor and the fit inner product are
-     reduced over *owned* rows only (rows touched by exactly one shard, and
-     shared rows owned by their lowest-rank toucher) — R, R x R and 1 values
-     per mode cross the interconnect.
+     reduced over *owned* rows only — R, R x R and 1 values per mode cross
+     the interconnect.
 
 All compute goes through an `ops` object: `DeviceOps` binds the B200 C ABI;
 tests inject CPU ops (gloo backend) to exercise the exchange logic.
@@ -39,8 +49,35 @@ def _torch():
     return torch
 
 
+def _p2p(sends, recvs, group=None):
+    """One grouped batch of point-to-point transfers (NCCL: ncclGroupStart /
+    ncclSend x k / ncclRecv x k / ncclGroupEnd).  gloo only moves host
+    tensors, so device buffers are staged through the host there."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    if not sends and not recvs:
+        return
+    stage = dist.get_backend(group) == "gloo"
+    ops, post = [], []
+    for t, peer in sends:
+        ops.append(dist.P2POp(dist.isend, t.cpu() if (stage and t.is_cuda) else t, peer, group))
+    for t, peer in recvs:
+        if stage and t.is_cuda:
+            h = torch.empty(t.shape, dtype=t.dtype)
+            ops.append(dist.P2POp(dist.irecv, h, peer, group))
+            post.append((t, h))
+        else:
+            ops.append(dist.P2POp(dist.irecv, t, peer, group))
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+    for t, h in post:
+        t.copy_(h)
+
+
 class ShardRows:
-    """Exchange plan of one mode: shared rows and this rank's owned-row mask."""
+    """Exchange plan of one mode: shared rows, owners, this rank's owned-row
+    mask, and the owner-directed send/receive row lists."""
 
     def __init__(self, touched, group=None):
         torch = _torch()
@@ -52,26 +89,137 @@ class ShardRows:
         dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
         first = torch.where(touched, torch.full_like(cnt, rank), torch.full_like(cnt, world))
         dist.all_reduce(first, op=dist.ReduceOp.MIN, group=group)
-        self.shared_rows = torch.nonzero(cnt >= 2).flatten().to(torch.int64)
+        shared = cnt >= 2
+        self.shared_rows = torch.nonzero(shared).flatten().to(torch.int64)
         self.owned = touched & ((cnt == 1) | (first == rank))
         self.mask = self.owned.to(torch.uint8)
         self.touched = touched
         self.group = group
+        self.rank, self.world = rank, world
+        # rows this rank sends to each owner (shared rows it touches but does not own)
+        mine = touched & shared & (first != rank)
+        rows = torch.nonzero(mine).flatten().to(torch.int64)
+        owner = first[rows].to(torch.int64)
+        self.send = {}
+        for o in range(world):
+            r = rows[owner == o]
+            if r.numel():
+                self.send[o] = r.contiguous()
+        # tell every owner how many rows (and which) each rank will send it
+        counts = torch.zeros(world, dtype=torch.int64, device=touched.device)
+        for o, r in self.send.items():
+            counts[o] = r.numel()
+        allc = [torch.zeros_like(counts) for _ in range(world)]
+        dist.all_gather(allc, counts, group=group)
+        self.recv = {}
+        recvs = []
+        for r_ in range(world):
+            n = int(allc[r_][rank].item())
+            if r_ != rank and n:
+                buf = torch.empty(n, dtype=torch.int64, device=touched.device)
+                self.recv[r_] = buf
+                recvs.append((buf, r_))
+        _p2p([(r, o) for o, r in self.send.items()], recvs, group)
 
     @property
     def n_shared(self) -> int:
         return int(self.shared_rows.numel())
 
+    def bytes_per_exchange(self, rank_r: int, elem_bytes: int) -> int:
+        """Bytes this rank sends + receives in one exchange (both legs)."""
+        rows = sum(int(r.numel()) for r in self.send.values()) + sum(int(r.numel()) for r in self.recv.values())
+        return 2 * rows * rank_r * elem_bytes
 
-def reduce_shared(out, plan: ShardRows, ops) -> None:
-    """Sum the partial rows of `out` that several shards touch (in place)."""
-    import torch.distributed as dist
 
-    if plan.n_shared == 0:
+def exchange_shared(out, plan: ShardRows, ops) -> None:
+    """Owner-directed shared-row reduction of `out` (in place): non-owners send
+    their partial rows to the owners, owners add them in rank order and send
+    the reduced rows back to exactly the ranks that touch them."""
+    torch = _torch()
+    if not plan.send and not plan.recv:
         return
-    buf = ops.pack(out, plan.shared_rows)
-    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=plan.group)
-    ops.unpack(out, plan.shared_rows, buf)
+    R = out.shape[1]
+    sends = [(ops.pack(out, rows), o) for o, rows in plan.send.items()]
+    rbufs = {r: torch.empty((rows.numel(), R), dtype=out.dtype, device=out.device) for r, rows in plan.recv.items()}
+    _p2p(sends, [(b, r) for r, b in rbufs.items()], plan.group)
+    for r in sorted(rbufs):
+        ops.add_rows(out, plan.recv[r], rbufs[r])
+    back = [(ops.pack(out, rows), r) for r, rows in plan.recv.items()]
+    bbufs = {o: torch.empty((rows.numel(), R), dtype=out.dtype, device=out.device) for o, rows in plan.send.items()}
+    _p2p(back, [(b, o) for o, b in bbufs.items()], plan.group)
+    for o, b in bbufs.items():
+        ops.unpack(out, plan.send[o], b)
+
+
+def build_shard(layout, coords, vals, rank: int, world: int, rank_r: int, sample: int = 1 << 22):
+    """This rank's key-range shard, cut by a cost model and built from its
+    own key range only (K1 on the given coordinates, K2 on the shard).
+
+    Cost of a key range = elements x (K + V) + sum_n rows_touched_n x R x S,
+    estimated on a strided sample whose elements weigh 1/count of their row
+    (full per-mode row counts).  Returns (AltoTensor, info)."""
+    torch = _torch()
+    from .format import AltoTensor
+    from .layout import linearize_device
+
+    m = int(coords.shape[0])
+    keys, bad = linearize_device(layout, coords)
+    nw = layout.n_words
+    kv = 8 * nw + vals.element_size()
+    rs = rank_r * vals.element_size()
+    step = max(1, m // sample)
+    idx = torch.arange(0, m, step, device=coords.device)
+    w = torch.full((idx.numel(),), float(kv) * step, dtype=torch.float64, device=coords.device)
+    for n, d in enumerate(layout.dims):
+        cnt = torch.bincount(coords[:, n], minlength=int(d)).to(torch.float64)
+        w += rs * step / cnt[coords[idx, n]]
+    sk = keys[idx]
+    flip = torch.tensor(-(1 << 63), dtype=torch.int64, device=keys.device)  # unsigned order via signed compare
+    if nw == 1:
+        order = torch.argsort(sk[:, 0] ^ flip, stable=True)
+    else:
+        order = torch.argsort(sk[:, 0] ^ flip, stable=True)
+        order = order[torch.argsort((sk[order, 1] ^ flip), stable=True)]
+    cw = torch.cumsum(w[order], 0)
+    total = float(cw[-1].item())
+    pos = [int(torch.searchsorted(cw, torch.tensor(total * g / world, dtype=torch.float64,
+                                                    device=cw.device)).item()) for g in range(1, world)]
+    cuts = [sk[order[min(p, order.numel() - 1)]] for p in pos]  # first key of shard g (g >= 1)
+
+    def ge(key_row):  # keys >= key_row (unsigned lexicographic, MS word last)
+        if nw == 1:
+            return (keys[:, 0] ^ flip) >= (key_row[0] ^ flip)
+        hi, lo = keys[:, 1] ^ flip, keys[:, 0] ^ flip
+        khi, klo = key_row[1] ^ flip, key_row[0] ^ flip
+        return (hi > khi) | ((hi == khi) & (lo >= klo))
+
+    sel = torch.ones(m, dtype=torch.bool, device=keys.device)
+    if rank > 0:
+        sel &= ge(cuts[rank - 1])
+    if rank < world - 1:
+        sel &= ~ge(cuts[rank])
+    skeys = keys[sel].contiguous()
+    svals = vals[sel].contiguous()
+    del keys
+    lib = _lib.load()
+    ms = int(skeys.shape[0])
+    ws_bytes = lib.alto_sort_workspace_bytes(ms, nw, svals.element_size())
+    wsb = torch.empty(max(int(ws_bytes), 8), dtype=torch.uint8, device=skeys.device)
+    _lib.check(lib.alto_sort_pairs(skeys.data_ptr(), svals.data_ptr(), ms, nw, svals.element_size(),
+                                   layout.total_bits, wsb.data_ptr(), ws_bytes, _lib.stream_ptr()), "alto_sort_pairs")
+    first = torch.empty(1, dtype=torch.int64, device=skeys.device)
+    _lib.check(lib.alto_find_duplicate(skeys.data_ptr(), ms, nw, first.data_ptr(), _lib.stream_ptr()),
+               "alto_find_duplicate")
+    flags = torch.stack([bad[0], first[0]]).cpu()
+    if int(flags[0]) >= 0:
+        raise ValueError("coordinates out of range for layout dims")
+    if int(flags[1]) >= 0:
+        raise ValueError("duplicate coordinates; coalesce the tensor first")
+    est = [float(cw[p - 1].item()) if p > 0 else 0.0 for p in pos]
+    bounds = [0.0] + est + [total]
+    info = {"nnz": ms, "cut": "cost-balanced key ranges (elements x (K+V) + touched rows x R x S)",
+            "est_cost_share": [(bounds[g + 1] - bounds[g]) / total for g in range(world)]}
+    return AltoTensor(layout, skeys, svals), info
 
 
 class DeviceOps:
@@ -111,6 +259,10 @@ class DeviceOps:
     def unpack(self, out, rows, buf):
         _lib.check(self.lib.alto_unpack_rows(out.data_ptr(), self._dt(out), rows.data_ptr(), rows.numel(),
                                              out.shape[1], buf.data_ptr(), _lib.stream_ptr()), "alto_unpack_rows")
+
+    def add_rows(self, out, rows, buf):
+        _lib.check(self.lib.alto_add_rows(out.data_ptr(), self._dt(out), rows.data_ptr(), rows.numel(),
+                                          out.shape[1], buf.data_ptr(), _lib.stream_ptr()), "alto_add_rows")
 
     def hadamard(self, grams, skip):
         from .cpd import hadamard_device
@@ -203,7 +355,7 @@ class ShardedCpAls:
 
     def mttkrp(self, mode: int):
         out = self.ops.mttkrp(self.fg, mode)
-        reduce_shared(out, self.plans[mode], self.ops)
+        exchange_shared(out, self.plans[mode], self.ops)
         return out
 
     def fit(self, m, mode: int) -> float:

@@ -2,8 +2,8 @@
 MTTKRP / CP-ALS exchange logic (paper_2102_10245_b200/dist.py).
 
 The per-shard compute is injected as CPU ops built on the oracle, so these
-tests exercise exactly the distributed part — shard plans, the shared-row
-all-reduce, owner-masked reductions — and compare against the single-process
+tests exercise exactly the distributed part — shard plans, the owner-directed
+shared-row exchange (grouped send/recv), owner-masked reductions — and compare against the single-process
 oracle (the reference algorithm).
 """
 
@@ -44,6 +44,9 @@ class CpuOps:
 
     def unpack(self, out, rows, buf):
         out.index_copy_(0, rows, buf)
+
+    def add_rows(self, out, rows, buf):
+        out.index_add_(0, rows, buf)
 
     def hadamard(self, grams, skip):
         v = torch.ones_like(grams[0])
@@ -114,6 +117,20 @@ def _worker(rank, world, port, case, outdir):
             touched_any[coords[:, n]] = 1
             assert dist_owned.numpy().tolist() == touched_any.tolist()  # every touched row owned exactly once
             del owned
+            # owner-directed lists: rank r sends exactly the shared rows it touches
+            # but does not own, each to its owner (the lowest-rank toucher)
+            mine = sorted(x for x in seen[rank] if x in set(shared))
+            want = {}
+            for x in mine:
+                o = min(r for r in range(world) if x in seen[r])
+                if o != rank:
+                    want.setdefault(o, []).append(x)
+            assert {o: r.tolist() for o, r in plan.send.items()} == want
+            got_recv = {r: v.tolist() for r, v in plan.recv.items()}
+            exp_recv = {r: sorted(x for x in seen[r] if x in set(shared) and x in seen[rank]
+                                  and min(q for q in range(world) if x in seen[q]) == rank)
+                        for r in range(world) if r != rank}
+            assert got_recv == {r: v for r, v in exp_recv.items() if v}
         # one sharded MTTKRP with the shared-row reduction == the global one
         m = solver.mttkrp(1)
         ref = orc.mttkrp_seq(lay, words, vals, [f.numpy() for f in solver.f64], 1)
@@ -130,11 +147,12 @@ def _worker(rank, world, port, case, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", [((60, 50, 40), 6000, 4, 3), ((30, 20, 25, 15), 4000, 3, 2)])
-def test_sharded_cpals_matches_single_process(case):
+@pytest.mark.parametrize("case,world", [(((60, 50, 40), 6000, 4, 3), 2), (((30, 20, 25, 15), 4000, 3, 2), 2),
+                                        (((60, 50, 40), 6000, 4, 2), 3)])
+def test_sharded_cpals_matches_single_process(case, world):
     dims, nnz, rank_r, iters = case
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(2, _free_port(), case, d), nprocs=2, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), case, d), nprocs=world, join=True)
         hist = np.load(os.path.join(d, "hist.npy"))
         st = synth.make_tensor(synth.SynthConfig("cfg8", dims, nnz, (("zipf", 1.1),) * len(dims), "uniform01",
                                                  "float64", rank_r), nnz=nnz, seed=77)
