@@ -411,11 +411,21 @@ int alto_mttkrp_exact(const alto_mttkrp_args* a, const int32_t* row_perm,
                       int64_t count, void* stream);
 
 /* COO MTTKRP over a coordinate list (mttkrp_oracle, mttkrp.py:64-77),
- * coords (M, order) int64, float64 atomics. */
+ * coords (M, order) int64, float64 atomics (not reproducible bit for bit). */
 int alto_mttkrp_coo(const int64_t* coords, const double* values, int64_t m,
                     int32_t order, int32_t mode, int32_t rank,
                     const double* const* factors_host_array /* host array of N device ptrs */,
                     double* out, int64_t out_rows, void* stream);
+/* The same in the reference's arithmetic order: elements stably sorted by
+ * output row, each row summed in input order (np.add.at, mttkrp.py:75) with
+ * contributions ((v * F_a) * F_b) ... in ascending mode order, float64, no
+ * contraction — bitwise equal to mttkrp_oracle.  Caller workspace of
+ * alto_mttkrp_coo_workspace_bytes(m, out_rows) bytes. */
+size_t alto_mttkrp_coo_workspace_bytes(int64_t m, int64_t out_rows);
+int alto_mttkrp_coo_ordered(const int64_t* coords, const double* values, int64_t m,
+                            int32_t order, int32_t mode, int32_t rank,
+                            const double* const* factors_host_array,
+                            double* out, int64_t out_rows, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- CP-ALS (cpd.py) --------------------------------------------------- */
 /* All reductions below are two-stage with a fixed block count, so results

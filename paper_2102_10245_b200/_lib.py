@@ -155,6 +155,9 @@ SIGNATURES = [
     ("alto_mttkrp_exact", c_int32, [POINTER(CMttkrpArgs), c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     ("alto_mttkrp_coo", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, POINTER(c_void_p),
                                   c_void_p, c_int64, c_void_p]),
+    ("alto_mttkrp_coo_workspace_bytes", c_size_t, [c_int64, c_int64]),
+    ("alto_mttkrp_coo_ordered", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, POINTER(c_void_p),
+                                          c_void_p, c_int64, c_void_p, c_size_t, c_void_p]),
     ("alto_cpd_workspace_bytes", c_size_t, [c_int32]),
     ("alto_gram", c_int32, [c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_hadamard_grams", c_int32, [POINTER(c_void_p), c_int32, c_int32, c_int32, c_void_p, c_void_p]),

@@ -132,6 +132,46 @@ __global__ void mttkrp_coo_kernel(const __grid_constant__ CooParams P) {
   }
 }
 
+// Input-order COO MTTKRP: rows sorted stably (element index as payload), one
+// warp per output row sums its elements in input order — np.add.at's order in
+// mttkrp_oracle (mttkrp.py:71-76), with contrib = ((v * F_a) * F_b) ... in
+// ascending mode order, no contraction: bitwise equal to the reference.
+__global__ void __launch_bounds__(256)
+mttkrp_coo_ordered_kernel(const __grid_constant__ CooParams P, const unsigned* __restrict__ perm,
+                          const long long* __restrict__ row_ptr, long long dim) {
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long row = gwarp; row < dim; row += nwarps) {
+    const long long j0 = row_ptr[row], j1 = row_ptr[row + 1];
+    for (int r0 = 0; r0 < P.rank; r0 += 32) {
+      const int r = r0 + lane;
+      double total = 0.0;
+      if (r < P.rank) {
+        for (long long j = j0; j < j1; ++j) {
+          const long long e = perm[j];
+          double x = P.values[e];
+          for (int n = 0; n < P.order; ++n) {
+            if (n == P.mode) continue;
+            x = __dmul_rn(x, P.factors[n][P.coords[e * P.order + n] * P.rank + r]);
+          }
+          total = __dadd_rn(total, x);
+        }
+        P.out[row * P.rank + r] = total;
+      }
+    }
+  }
+}
+
+__global__ void coo_rows_kernel(const long long* __restrict__ coords, long long m, int order, int mode,
+                                uint64_t* __restrict__ rows, unsigned* __restrict__ idx) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m; i += stride) {
+    rows[i] = static_cast<uint64_t>(coords[i * order + mode]);
+    idx[i] = static_cast<unsigned>(i);
+  }
+}
+
 // ---- launch helpers ----------------------------------------------------------------
 
 template <typename K>
@@ -238,6 +278,57 @@ int alto_mttkrp_exact(const alto_mttkrp_args* a, const int32_t* row_perm, const 
   if (!v32 && !f32) return go(mttkrp_exact_kernel<2, double, double>);
   if (v32) return go(mttkrp_exact_kernel<2, float, double>);
   return go(mttkrp_exact_kernel<2, double, float>);
+}
+
+size_t alto_mttkrp_coo_workspace_bytes(int64_t m, int64_t out_rows) {
+  if (m < 0) m = 0;
+  const size_t a = (static_cast<size_t>(m) * 8 + 255) & ~size_t(255);
+  const size_t b = (static_cast<size_t>(m) * 4 + 255) & ~size_t(255);
+  const size_t c = (static_cast<size_t>(out_rows + 1) * 8 + 255) & ~size_t(255);
+  return a + b + c + alto_sort_workspace_bytes(m, 1, 4);
+}
+
+int alto_mttkrp_coo_ordered(const int64_t* coords, const double* values, int64_t m, int32_t order, int32_t mode,
+                            int32_t rank, const double* const* factors_host_array, double* out, int64_t out_rows,
+                            void* ws, size_t ws_bytes, void* stream) {
+  ALTO_REQUIRE(order >= 1 && order <= ALTO_MAX_ORDER, "order out of range");
+  ALTO_REQUIRE(mode >= 0 && mode < order, "mode out of range");
+  ALTO_REQUIRE(rank >= 1, "rank must be positive");
+  ALTO_REQUIRE(m < (1ll << 32) - 1, "ordered COO MTTKRP supports fewer than 2^32 elements");
+  cudaStream_t s = as_stream(stream);
+  if (m <= 0) {
+    ALTO_CUDA_TRY(cudaMemsetAsync(out, 0, static_cast<size_t>(out_rows) * rank * sizeof(double), s));
+    return ALTO_OK;
+  }
+  ALTO_REQUIRE(ws && ws_bytes >= alto_mttkrp_coo_workspace_bytes(m, out_rows), "COO workspace too small");
+  const size_t a = (static_cast<size_t>(m) * 8 + 255) & ~size_t(255);
+  const size_t b = (static_cast<size_t>(m) * 4 + 255) & ~size_t(255);
+  const size_t c = (static_cast<size_t>(out_rows + 1) * 8 + 255) & ~size_t(255);
+  auto* rows = static_cast<uint64_t*>(ws);
+  auto* idx = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + a);
+  auto* row_ptr = reinterpret_cast<long long*>(static_cast<char*>(ws) + a + b);
+  void* sws = static_cast<char*>(ws) + a + b + c;
+  const auto* cc = reinterpret_cast<const long long*>(coords);
+  coo_rows_kernel<<<grid_for(m, 256), 256, 0, s>>>(cc, m, order, mode, rows, idx);
+  ALTO_LAUNCH_CHECK("alto_mttkrp_coo_ordered/rows");
+  int bits = 1;
+  while (bits < 63 && (1ll << bits) < out_rows) ++bits;
+  const int st = alto_sort_pairs(rows, idx, m, 1, 4, bits, sws, ws_bytes - a - b - c, stream);
+  if (st) return st;
+  row_ptr_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(rows, m, out_rows, row_ptr);
+  ALTO_LAUNCH_CHECK("alto_mttkrp_coo_ordered/row_ptr");
+  CooParams P{};
+  P.coords = cc;
+  P.values = values;
+  P.m = m;
+  P.order = order;
+  P.mode = mode;
+  P.rank = rank;
+  for (int n = 0; n < order; ++n) P.factors[n] = factors_host_array[n];
+  P.out = out;
+  mttkrp_coo_ordered_kernel<<<grid_for(out_rows * 32, 256, kSMs * 64), 256, 0, s>>>(P, idx, row_ptr, out_rows);
+  ALTO_LAUNCH_CHECK("alto_mttkrp_coo_ordered");
+  return ALTO_OK;
 }
 
 int alto_mttkrp_coo(const int64_t* coords, const double* values, int64_t m, int32_t order, int32_t mode,

@@ -171,21 +171,18 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
 
   const long long base = tile * kSortTile + static_cast<long long>(warp) * kWarpSlice;
   const unsigned lt_mask = (1u << lane) - 1u;
-  Key<W> k[kSortItems];
-  uint64_t pv[kSortItems];
-  unsigned rank[kSortItems];
-  unsigned dig[kSortItems];
+  // Ranking pass: only the key word holding the digit is read; each item
+  // keeps (rank << 8 | digit) in one register (ranks < 4096), so the kernel
+  // stays small enough for several CTAs per SM; keys and payload are re-read
+  // (L2 hits) in the placement pass below.
+  const int dw = shift >> 6;
+  unsigned rd[kSortItems];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const long long i = base + j * 32 + lane;
     const bool valid = i < m;
-    if (valid) {
-      k[j] = load_key<W>(keys_in, i);
-      if constexpr (P == 4) pv[j] = static_cast<const unsigned*>(pay_in)[i];
-      if constexpr (P == 8) pv[j] = static_cast<const uint64_t*>(pay_in)[i];
-    }
-    const unsigned d = valid ? digit_of<W>(k[j], shift) : 0x100u + lane;  // invalid lanes: singleton groups
-    dig[j] = d;
+    unsigned d = 0x100u + lane;  // invalid lanes: singleton groups
+    if (valid) d = static_cast<unsigned>(__ldg(keys_in + i * W + dw) >> (shift & 63)) & 0xffu;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const unsigned r = __popc(peers & lt_mask);
     unsigned prior = 0;
@@ -193,7 +190,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
     __syncwarp();
     if (valid && r == 0) s_warp[warp][d] = prior + __popc(peers);
     __syncwarp();
-    rank[j] = prior + r;
+    rd[j] = ((prior + r) << 8) | (d & 0xffu);
   }
   __syncthreads();
   {
@@ -216,16 +213,17 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
   for (int j = 0; j < kSortItems; ++j) {
     const long long i = base + j * 32 + lane;
     if (i < m) {
-      const unsigned d = dig[j];
-      const unsigned lp = s_dstart[d] + s_warp[warp][d] + rank[j];
+      const unsigned d = rd[j] & 0xffu;
+      const unsigned lp = s_dstart[d] + s_warp[warp][d] + (rd[j] >> 8);
+      const Key<W> k = load_key<W>(keys_in, i);
       if constexpr (W == 1) {
-        s_keys[lp] = k[j].w[0];
+        s_keys[lp] = k.w[0];
       } else {
-        s_keys[2 * lp] = k[j].w[0];
-        s_keys[2 * lp + 1] = k[j].w[1];
+        s_keys[2 * lp] = k.w[0];
+        s_keys[2 * lp + 1] = k.w[1];
       }
-      if constexpr (P == 4) s_pay32[lp] = static_cast<unsigned>(pv[j]);
-      if constexpr (P == 8) s_pay64[lp] = pv[j];
+      if constexpr (P == 4) s_pay32[lp] = static_cast<const unsigned*>(pay_in)[i];
+      if constexpr (P == 8) s_pay64[lp] = static_cast<const uint64_t*>(pay_in)[i];
     }
   }
   __syncthreads();

@@ -391,9 +391,7 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
         ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
         rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals), m,
                                   mode, T, MS_ORDER | (4 if MS_RR else 0), hs[0].data_ptr() if hot else None,
-                                  skeys.data_ptr(),
-                                  svals.data_ptr(),
-                                  ws.data_ptr(), wsb, _lib.stream_ptr())
+                                  skeys.data_ptr(), svals.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr())
         del ws
         if rc == _lib.ALTO_EUNSUPPORTED:
             hit = False  # field layout does not fit the key width: planned kernel instead
@@ -882,18 +880,25 @@ def _finish(out_dev, like_torch: bool):
 
 
 def mttkrp_oracle(tensor: CooTensor, factors, mode: int):
-    """COO MTTKRP (mttkrp.py:64-77) on the device, float64 atomics."""
+    """COO MTTKRP (mttkrp.py:64-77) on the device in the reference's order:
+    each output row sums its elements in input order (np.add.at), products in
+    ascending mode order, float64 without contraction — bitwise equal to the
+    reference (alto_mttkrp_coo_ordered)."""
     torch = _torch()
     rank = _check_factors(tensor.dims, factors, mode)
     dev = _lib.cuda_device()
-    out = torch.empty((tensor.dims[mode], rank), dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    dim = tensor.dims[mode]
+    out = torch.empty((dim, rank), dtype=torch.float64, device=dev)
     fdev = factors_to_device(factors, torch.float64, skip=mode)
-    coords = torch.from_numpy(tensor.coords).to(dev)
-    vals = torch.from_numpy(tensor.values).to(dev)
+    coords = torch.from_numpy(np.ascontiguousarray(tensor.coords, dtype=np.int64)).to(dev)
+    vals = torch.from_numpy(np.ascontiguousarray(tensor.values, dtype=np.float64)).to(dev)
     arr = (ctypes.c_void_p * len(fdev))(*[f.data_ptr() for f in fdev])
-    _lib.check(_lib.load().alto_mttkrp_coo(coords.data_ptr(), vals.data_ptr(), tensor.nnz, tensor.order, mode, rank,
-                                           arr, out.data_ptr(), tensor.dims[mode], _lib.stream_ptr()),
-               "alto_mttkrp_coo")
+    wsb = int(lib.alto_mttkrp_coo_workspace_bytes(tensor.nnz, dim))
+    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+    _lib.check(lib.alto_mttkrp_coo_ordered(coords.data_ptr(), vals.data_ptr(), tensor.nnz, tensor.order, mode, rank,
+                                           arr, out.data_ptr(), dim, ws.data_ptr(), wsb, _lib.stream_ptr()),
+               "alto_mttkrp_coo_ordered")
     return _finish(out, any(_is_torch(f) for f in factors))
 
 

@@ -54,7 +54,7 @@ def test_engines_match_reference(at, name):
     for mode in range(len(meta["dims"])):
         # exact-order engine == reference mttkrp_seq, bit for bit
         compare(data, meta, f"m{mode}_seq", at.mttkrp_seq(alto, factors, mode), 0)
-        compare(data, meta, f"m{mode}_oracle", at.mttkrp_oracle(coo, factors, mode), 1e-12)
+        compare(data, meta, f"m{mode}_oracle", at.mttkrp_oracle(coo, factors, mode), 0)
         for count in meta["counts"]:
             parts = at.partition(alto, count)
             plan = at.plan_conflicts(alto, parts, mode, force_strategy=at.Strategy.BUFFERED)
@@ -560,3 +560,19 @@ def test_live_reference_bitwise(at, cfg, nnz):
         d_plan = at.plan_conflicts(d_alto, d_parts, mode, force_strategy=at.Strategy.BUFFERED)
         got = at.mttkrp_par(d_alto, d_parts, d_plan, factors, mode, workers=4)
         assert np.array_equal(got, want), (cfg, mode, rel_error(got, want))
+
+
+@pytest.mark.parametrize("cfg,nnz", [(2, 300_000), (4, 200_000), (3, 100_000)])
+def test_device_oracle_bitwise_vs_c_oracle(at, cfg, nnz):
+    """The drop-in mttkrp_oracle accumulates in input order (np.add.at,
+    mttkrp.py:75): bit for bit the C oracle, which is pinned to the reference."""
+    from oracle import oracle_c
+
+    st = synth.make_tensor(cfg, nnz=nnz)
+    dims, rank = st.config.dims, st.config.rank
+    coo = at.CooTensor(dims, st.coords, st.values.astype(np.float64))
+    factors = seeded_factors(dims, rank, seed=cfg)
+    for mode in range(len(dims)):
+        got = at.mttkrp_oracle(coo, factors, mode)
+        want = oracle_c.mttkrp_coo(st.coords, st.values.astype(np.float64), factors, mode)
+        assert np.array_equal(got, want), (cfg, mode)
