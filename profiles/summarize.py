@@ -19,7 +19,7 @@ import subprocess
 import sys
 
 
-STEP_KERNELS = ("mstream_kernel<1, float, float, 3, 16", "hot_reduce_rows_kernel<float>")
+STEP_KERNELS = ("mstream_kernel<", "hot_reduce_rows_kernel<float>")
 
 
 def launches(path: str, out: str) -> None:
