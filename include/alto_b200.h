@@ -173,13 +173,6 @@ typedef struct alto_mttkrp_args {
    * in-tile sort. */
   const uint64_t* packed;
   const uint8_t* pos;
-  /* Plan 2 (preferred over `pos` when set): per-mode 64-bit plan words from
-   * alto_stream_plan and, for up to 3 input modes (mode order, output mode
-   * skipped), the ids of `cache_k` hot rows staged in shared memory. */
-  const uint64_t* plan;
-  const int32_t* cache_rows[3];
-  int32_t cache_k;
-  int32_t cache_modes;
   const double* fixed_scale;     /* device scalar for ALTO_I64 output (alto_fixed_scale) */
   /* Per-mode stream (built by alto_mode_stream for this mode): keys, values
    * and its tile length.  When set, the mode-stream kernel runs (orders 3-5,
@@ -204,6 +197,9 @@ typedef struct alto_mttkrp_args {
   int32_t pair_a[2];
   int32_t pair_b[2];
   const void* pair_tab[2];
+  /* Delta mode stream (alto_mode_stream with ALTO_MS_DELTA): the row of each
+   * lane group's first element (ntiles * 8 int32); NULL for plain streams. */
+  const int32_t* mbase;
 } alto_mttkrp_args;
 
 /* Row-wise (Khatri-Rao) product table of two factors for paired input modes:
@@ -224,24 +220,14 @@ int alto_fixed_scale(const double* terms, int32_t nterms, double* scale, void* s
 int alto_fixed_to_float(const int64_t* in, const double* scale, void* out, int32_t out_dtype, int64_t n,
                         void* stream);
 
-/* Top-k rows of a mode by element count (from alto_row_index's row_ptr):
- * rows (k int32, -1 padded) and slot_map (dim int32: slot or -1). */
+/* Workspace of alto_hot_rows (a sort of the mode's dim row counts). */
 size_t alto_topk_rows_workspace_bytes(int64_t dim);
-int alto_topk_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int32_t* rows, int32_t* slot_map, void* ws,
-                   size_t ws_bytes, void* stream);
 /* Hot-row plan by rank: the (up to) k rows with the most elements, keeping
  * only rows with more than min_count; slots 0..*d_count-1 in descending
- * count order (rows -1 padded; slot_map dim int32: slot or -1).  Same
- * workspace as alto_topk_rows. */
+ * count order (rows -1 padded; slot_map dim int32: slot or -1); workspace
+ * of alto_topk_rows_workspace_bytes(dim) bytes. */
 int alto_hot_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int64_t min_count, int32_t* rows,
                   int32_t* slot_map, int32_t* d_count, void* ws, size_t ws_bytes, void* stream);
-/* Per-mode plan words (see alto_fast.cuh, planned variant 2): slot in the
- * 256-element sub-tile after a stable counting sort by `mode` coordinate,
- * hot-input slots for up to 3 input modes (in_slot_maps_host: host array of
- * `order` device pointers, entries may be NULL) and hot output slot + 1. */
-int alto_stream_plan(const alto_layout* lay, const uint64_t* packed, int64_t m, int32_t mode,
-                     const int32_t* const* in_slot_maps_host, const int32_t* hot_out_slot, uint64_t* plan,
-                     void* stream);
 
 /* Mode-contiguous re-encoding of sorted ALTO keys: packed[i] holds mode n's
  * coordinate in bits [sum_{m<n} b_m, +b_n) (same n_words as the keys). */
@@ -271,9 +257,16 @@ size_t alto_mode_stream_workspace_bytes(int64_t m);
                                within a row), not tile by tile */
 #define ALTO_MS_ROUND_ROBIN 4 /* flags: lane group s of a tile takes sorted positions s, s+8, ... (stream
                                  stored in sorted order) instead of a contiguous slice */
+#define ALTO_MS_DELTA 8 /* flags (row-major only): one 64-bit key word per element — the input
+                           coordinates plus the row increment from the previous element of the same
+                           lane group (base_rows[tile * 8 + group] holds each group's first row);
+                           ALTO_EUNSUPPORTED if fewer than 8 increment bits are left, and
+                           *d_overflow (device int32, zeroed by the call) is set when an increment
+                           does not fit (the caller then builds a plain stream) */
 int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,
                      int64_t m, int32_t mode, int32_t tile, int32_t flags, const int32_t* hot_slot,
-                     uint64_t* skeys, void* svals, void* ws, size_t ws_bytes, void* stream);
+                     uint64_t* skeys, void* svals, int32_t* base_rows, int32_t* d_overflow,
+                     void* ws, size_t ws_bytes, void* stream);
 
 /* Hot-row copy plan of the mode-stream kernel: hot row s (hot_rows[s],
  * from alto_hot_rows) gets copies = 2^lg replicated partial rows, lg the
@@ -303,13 +296,8 @@ int alto_coalesce(const int64_t* coords, const double* values, int64_t m, int32_
 #define ALTO_STREAM_CTA_TILES 4  /* CTA-wide 1024-element tiles (cp.async staged)
                                     instead of warp-autonomous 128-element tiles */
 #define ALTO_STREAM_GENERIC 128  /* bypass the specialised (order 3-5, rank 16/32) kernels */
-#define ALTO_STREAM_TUNE_MINB2 256  /* tuning: planned kernel: 2 CTAs/SM launch bounds (default 3);
-                                       mode-stream kernel (cfg2 shape): shuffle raw keys */
-#define ALTO_STREAM_TUNE_U4 512     /* tuning: planned kernel: 4 elements in flight per group (default 2);
-                                       mode-stream kernel (cfg2 shape): record exchange through shared
-                                       memory instead of shuffles */
-#define ALTO_STREAM_MS_COOP 1024    /* tuning: mode-stream kernel with broadcast key loads instead of
-                                       cooperative decode + shuffles (cfg2 shape only) */
+#define ALTO_STREAM_TUNE_MINB2 256  /* tuning: planned kernel: 2 CTAs/SM launch bounds (default 3) */
+#define ALTO_STREAM_TUNE_U4 512     /* tuning: planned kernel: 4 elements in flight per group (default 2) */
 #define ALTO_STREAM_MS_L2_NORMAL 2048 /* tuning: mode-stream loads without the L2 evict_first policy */
 /* Ablation switches for profiling only (results are wrong when set). */
 #define ALTO_STREAM_DBG_NO_RED 8

@@ -57,10 +57,6 @@ class CMttkrpArgs(Structure):
         ("flags", c_int32),
         ("packed", c_void_p),
         ("pos", c_void_p),
-        ("plan", c_void_p),
-        ("cache_rows", c_void_p * 3),
-        ("cache_k", c_int32),
-        ("cache_modes", c_int32),
         ("fixed_scale", c_void_p),
         ("mkeys", c_void_p),
         ("mvals", c_void_p),
@@ -71,6 +67,7 @@ class CMttkrpArgs(Structure):
         ("pair_a", c_int32 * 2),
         ("pair_b", c_int32 * 2),
         ("pair_tab", c_void_p * 2),
+        ("mbase", c_void_p),
     ]
 
 
@@ -138,13 +135,11 @@ SIGNATURES = [
     ("alto_hot_copies", c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p,
                                   c_void_p, c_void_p]),
     ("alto_mode_stream", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32,
-                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                   c_void_p]),
     ("alto_topk_rows_workspace_bytes", c_size_t, [c_int64]),
-    ("alto_topk_rows", c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     ("alto_hot_rows", c_int32, [c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_size_t, c_void_p]),
-    ("alto_stream_plan", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, POINTER(c_void_p), c_void_p,
-                                   c_void_p, c_void_p]),
     ("alto_hot_plan", c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("alto_row_index_workspace_bytes", c_size_t, [c_int64, c_int64]),
     ("alto_row_index", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,

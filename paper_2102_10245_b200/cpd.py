@@ -25,9 +25,9 @@ from .mttkrp import (F32_ACCUMULATE, _check_factors, factors_to_device, mttkrp_d
 
 BACKENDS = ("seq", "oracle", "auto", "buffered", "atomic")
 # Replay the per-mode updates of a sweep as one CUDA graph (after the first sweep)
-CPD_GRAPHS = __import__("os").environ.get("ALTO_CPD_GRAPHS", "1") == "1"
+CPD_GRAPHS = True
 # alto_cpd_update flags (ALTO_CPD_SCALAR = 1: scalar substitution instead of the rank-16 DMMA path)
-CPD_UPDATE_FLAGS = int(__import__("os").environ.get("ALTO_CPD_FLAGS", "0"))
+CPD_UPDATE_FLAGS = 0
 
 
 def _torch():

@@ -375,9 +375,6 @@ int try_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packe
                 cudaStream_t s);
 template <int W, typename V, typename O>
 int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s);
-struct Plan2;
-template <int W, typename V, typename O>
-int try_planned2(const DevLayout& d, const StreamParams& P, const Plan2& PL, cudaStream_t s);
 
 template <int W, typename V, typename O>
 int try_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaStream_t s) {
@@ -387,10 +384,6 @@ int try_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cud
     const int st = try_mstream<W, V, O>(d, P, s);
     if (st == ALTO_EUNSUPPORTED) set_error("shape not covered by the mode-stream kernel");
     return st;
-  }
-  if (P.packed && P.plan2 && P.plan2->plan) {
-    const int st = try_planned2<W, V, O>(d, P, *P.plan2, s);
-    if (st != ALTO_EUNSUPPORTED) return st;
   }
   if (P.packed && P.pos) {
     const int st = try_planned<W, V, O>(d, P, P.packed, P.pos, s);
@@ -665,288 +658,6 @@ int try_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packe
     if (d.order == 3) return launch_planned<W, V, O, 3, 32>(d, P, packed, pos, s);
     if (d.order == 4) return launch_planned<W, V, O, 4, 32>(d, P, packed, pos, s);
     if (d.order == 5) return launch_planned<W, V, O, 5, 32>(d, P, packed, pos, s);
-  }
-  return ALTO_EUNSUPPORTED;
-}
-
-
-// ---- planned variant 2: per-mode 64-bit plan words + shared hot-input rows ----
-// plan[e] (uint64, per mode, built by alto_stream_plan):
-//   bits  0- 7  slot of e in its 256-element sub-tile (stable row-sorted)
-//   bits  8-31  for input modes k = 0..2: slot in the CTA's hot-input row
-//               cache (the mode's top rows by element count), 255 = cold
-//   bits 32-47  hot output slot + 1 (0 = not a hot row)
-// Phase A needs only the packed key, the value and the plan word (no table,
-// no sort, no lookup); phase B reads hot input rows from shared memory
-// (LDS.128) and cold ones from global memory.
-constexpr int kPlanTile = 256;
-constexpr int kMaxCacheModes = 3;
-
-struct Plan2 {
-  const unsigned long long* plan;
-  const int* cache_rows[kMaxCacheModes];  // per input mode k: K row ids
-  int cache_k;                            // rows cached per input mode
-  int cache_modes;                        // input modes with a cache (<= 3)
-};
-
-template <int W, typename V, typename O, int N, int R, int MINB = 3, int UF = 2>
-__global__ void __launch_bounds__(kTileThreads, MINB)
-planned2_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ packed,
-                const __grid_constant__ Plan2 PL, const __grid_constant__ StreamParams P) {
-  using F = V;
-  using A = V;
-  constexpr int G = R / 4;
-  constexpr int GPW = 32 / G;
-  constexpr int CH = kPlanTile / GPW;
-  constexpr int NIN = N - 1;
-  using RL = RecLayout<N, V>;
-  constexpr int NW = RL::NW;
-  constexpr int EPL = kPlanTile / 32;
-  constexpr int U = UF;
-  constexpr int REC_WORDS = kPlanTile * NW + GPW * 4;
-  constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
-  constexpr unsigned HOTBIT = 0x80000000u;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int mode = P.mode;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = PL.cache_k;
-  const int CM = PL.cache_modes;
-  unsigned char* s_cache = smem;  // CM x K rows
-  const size_t cache_bytes = (static_cast<size_t>(CM) * K * ROWB + 15) & ~size_t(15);
-  unsigned* s_rec = reinterpret_cast<unsigned*>(smem + cache_bytes) + warp * REC_WORDS;
-  const F* fbase[NIN];
-#pragma unroll
-  for (int k = 0; k < NIN; ++k) {
-    const int n = k < mode ? k : k + 1;
-    fbase[k] = static_cast<const F*>(P.factors[n]);
-  }
-  // stage the hot input rows of this call's factors (16-byte chunks)
-  {
-    const int chunks = ROWB / 16;
-    for (int t = threadIdx.x; t < CM * K * chunks; t += blockDim.x) {
-      const int k = t / (K * chunks);
-      const int rem = t - k * K * chunks;
-      const int srow = rem / chunks, c = rem - srow * chunks;
-      const int grow = PL.cache_rows[k][srow];
-      const float4 v = grow >= 0 ? __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(fbase[k]) +
-                                                                        static_cast<long long>(grow) * ROWB) + c)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-      reinterpret_cast<float4*>(s_cache + (static_cast<size_t>(k) * K + srow) * ROWB)[c] = v;
-    }
-  }
-  __syncthreads();
-  const int grp = lane / G;
-  const int gl = lane % G;
-  const unsigned qmask = (G >= 4) ? (0xFu << (lane & ~3)) : 0xffffffffu;
-  const char* gbase_lane[NIN];
-#pragma unroll
-  for (int k = 0; k < NIN; ++k) gbase_lane[k] = reinterpret_cast<const char*>(fbase[k] + 4 * gl);
-  const unsigned char* sbase_lane = s_cache + 4 * gl * sizeof(F);
-  int pack_off[N], bits[N];
-#pragma unroll
-  for (int n = 0; n < N; ++n) { pack_off[n] = L.pack_off[n]; bits[n] = L.bits[n]; }
-  const V* __restrict__ vals = static_cast<const V*>(P.values);
-  O* __restrict__ out = static_cast<O*>(P.out);
-  const double fixed_scale = P.fixed_scale ? *P.fixed_scale : 1.0;
-  auto rec_addr = [](int j) { return j * NW + (j / CH) * 4; };
-
-  const long long nsub = (P.m + kPlanTile - 1) / kPlanTile;
-  const long long gw0 = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp;
-  const long long nwarps = static_cast<long long>(gridDim.x) * (kTileThreads / 32);
-  for (long long sub = gw0; sub < nsub; sub += nwarps) {
-    const long long e0 = sub * kPlanTile;
-    const int cnt = static_cast<int>(min(static_cast<long long>(kPlanTile), P.m - e0));
-    // ---- phase A: stream, decode by shifts, scatter records to planned slots --
-#pragma unroll
-    for (int k = 0; k < EPL; ++k) {
-      const int e = lane + 32 * k;
-      if (e < cnt) {
-        const Key<W> key = load_key<W>(packed, e0 + e);
-        const V v = __ldg(vals + e0 + e);
-        const unsigned long long pw = __ldg(PL.plan + e0 + e);
-        unsigned c[N];
-#pragma unroll
-        for (int n = 0; n < N; ++n) c[n] = packed_field32<W>(key, pack_off[n], bits[n]);
-        unsigned rec[NW];
-#pragma unroll
-        for (int q = 0; q < NIN; ++q) {
-          const unsigned cq = (q < mode) ? c[q] : c[q + 1];
-          const unsigned h = q < kMaxCacheModes ? static_cast<unsigned>(pw >> (8 + 8 * q)) & 0xffu : 0xffu;
-          rec[q] = (h != 0xffu && q < CM) ? (HOTBIT | ((static_cast<unsigned>(q) * K + h) * ROWB))
-                                          : cq * (ROWB / 16);
-        }
-        unsigned row = c[0];
-#pragma unroll
-        for (int n = 1; n < N; ++n)
-          if (n == mode) row = c[n];
-        const unsigned hot1 = P.n_hot > 0 ? static_cast<unsigned>(pw >> 32) & 0xffffu : 0u;
-        rec[RL::TGT] = hot1 ? static_cast<unsigned>(-static_cast<int>(hot1)) : row;
-        if constexpr (sizeof(V) == 4) {
-          rec[RL::VAL] = __float_as_uint(v);
-        } else {
-          const unsigned long long u = __double_as_longlong(v);
-          rec[RL::VAL] = static_cast<unsigned>(u);
-          rec[RL::VAL + 1] = static_cast<unsigned>(u >> 32);
-        }
-#pragma unroll
-        for (int q = RL::raw; q < NW; ++q) rec[q] = 0u;
-        const int slot = static_cast<int>(pw & 0xffu);
-#pragma unroll
-        for (int q = 0; q < NW; q += 4)
-          *reinterpret_cast<uint4*>(s_rec + rec_addr(slot) + q) = make_uint4(rec[q], rec[q + 1], rec[q + 2], rec[q + 3]);
-      }
-    }
-    __syncwarp();
-    // ---- phase B ---------------------------------------------------------------
-    O* hot_base = P.n_hot > 0 ? static_cast<O*>(P.hot_buf) +
-                                    static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) *
-                                        P.n_hot * R
-                              : nullptr;
-    A acc[4] = {A(0), A(0), A(0), A(0)};
-    int cur = INT_MIN;
-    auto flush = [&]() {
-      O* base = cur >= 0 ? out + static_cast<long long>(cur) * R : hot_base + static_cast<long long>(-cur - 1) * R;
-      merge_row<O, A, G, R>(base, acc, gl, qmask, lane, fixed_scale);
-    };
-    // hot input row -> shared-memory cache, cold row -> read-only global path;
-    // both loads sit in one predicated asm block (no branch), so the U x NIN
-    // gathers stay in flight together and each lane pays only its own path
-    const unsigned s_cache_u32 = static_cast<unsigned>(__cvta_generic_to_shared(sbase_lane));
-    auto fetch = [&](int k, unsigned w) -> V4<F> {
-      V4<F> o;
-      const unsigned saddr = s_cache_u32 + (w & ~HOTBIT);
-      const char* gaddr = gbase_lane[k] + static_cast<unsigned long long>(w) * 16u;
-      const unsigned hot = w >> 31;
-      if constexpr (sizeof(F) == 4) {
-        float a, b, c, e;
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
-            " @p ld.shared.v4.f32 {%0, %1, %2, %3}, [%5];\n"
-            " @!p ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%6];\n}\n"
-            : "=f"(a), "=f"(b), "=f"(c), "=f"(e)
-            : "r"(hot), "r"(saddr), "l"(gaddr));
-        o.v[0] = a; o.v[1] = b; o.v[2] = c; o.v[3] = e;
-      } else {
-        double a, b, c, e;
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
-            " @p ld.shared.v2.f64 {%0, %1}, [%5];\n"
-            " @p ld.shared.v2.f64 {%2, %3}, [%5+16];\n"
-            " @!p ld.global.nc.v2.f64 {%0, %1}, [%6];\n"
-            " @!p ld.global.nc.v2.f64 {%2, %3}, [%6+16];\n}\n"
-            : "=d"(a), "=d"(b), "=d"(c), "=d"(e)
-            : "r"(hot), "r"(saddr), "l"(gaddr));
-        o.v[0] = a; o.v[1] = b; o.v[2] = c; o.v[3] = e;
-      }
-      return o;
-    };
-    auto consume = [&](const unsigned (&cw)[NW], const V4<F> (&g)[NIN]) {
-      const int tg = static_cast<int>(cw[RL::TGT]);
-      A v;
-      if constexpr (sizeof(V) == 4) {
-        v = __uint_as_float(cw[RL::VAL]);
-      } else {
-        v = __longlong_as_double(
-            static_cast<long long>((static_cast<unsigned long long>(cw[RL::VAL + 1]) << 32) | cw[RL::VAL]));
-      }
-      A t[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) t[q] = v * static_cast<A>(g[0].v[q]);
-#pragma unroll
-      for (int k = 1; k < NIN - 1; ++k)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) t[q] *= static_cast<A>(g[k].v[q]);
-      if (tg == cur) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = fma(t[q], static_cast<A>(g[NIN - 1].v[q]), acc[q]);
-      } else {
-        if (cur != INT_MIN) flush();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = t[q] * static_cast<A>(g[NIN - 1].v[q]);
-        cur = tg;
-      }
-    };
-    const int j0 = grp * CH;
-    if (cnt == kPlanTile) {
-#pragma unroll 1
-      for (int jb = j0; jb < j0 + CH; jb += U) {
-        unsigned cw[U][NW];
-        V4<F> g[U][NIN];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-          for (int q = 0; q < NW; q += 4) {
-            const uint4 t = *reinterpret_cast<const uint4*>(s_rec + rec_addr(jb + u) + q);
-            cw[u][q] = t.x; cw[u][q + 1] = t.y; cw[u][q + 2] = t.z; cw[u][q + 3] = t.w;
-          }
-#pragma unroll
-          for (int k = 0; k < NIN; ++k) g[u][k] = fetch(k, cw[u][k]);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) consume(cw[u], g[u]);
-      }
-    } else {
-      const int j1 = min(cnt, j0 + CH);
-#pragma unroll 1
-      for (int j = j0; j < j1; ++j) {
-        unsigned cw[NW];
-        V4<F> g[NIN];
-#pragma unroll
-        for (int q = 0; q < NW; q += 4) {
-          const uint4 t = *reinterpret_cast<const uint4*>(s_rec + rec_addr(j) + q);
-          cw[q] = t.x; cw[q + 1] = t.y; cw[q + 2] = t.z; cw[q + 3] = t.w;
-        }
-#pragma unroll
-        for (int k = 0; k < NIN; ++k) g[k] = fetch(k, cw[k]);
-        consume(cw, g);
-      }
-    }
-    if (cur != INT_MIN) flush();
-    __syncwarp();
-  }
-}
-
-template <int W, typename V, typename O, int N, int R>
-int launch_planned2(const DevLayout& d, const StreamParams& P, const Plan2& PL, cudaStream_t s) {
-  constexpr int NW = RecLayout<N, V>::NW;
-  constexpr int GPW = 32 / (R / 4);
-  const size_t cache = (static_cast<size_t>(PL.cache_modes) * PL.cache_k * R * sizeof(V) + 15) & ~size_t(15);
-  const size_t smem = cache + (kTileThreads / 32) * (static_cast<size_t>(kPlanTile) * NW + GPW * 4) * 4;
-  auto kern = planned2_kernel<W, V, O, N, R>;
-  static size_t cached_smem = 0;
-  static int cached_bps = 0;
-  if (cached_smem != smem) {
-    if (prep(kern, smem)) return ALTO_ECUDA;
-    int b = 1;
-    ALTO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kTileThreads, smem));
-    cached_bps = b;
-    cached_smem = smem;
-  }
-  const long long nsub = (P.m + kPlanTile - 1) / kPlanTile;
-  const long long need = (nsub + kTileThreads / 32 - 1) / (kTileThreads / 32);
-  const long long grid = std::min<long long>(need, static_cast<long long>(device_sms()) * std::max(cached_bps, 1));
-  kern<<<static_cast<unsigned>(grid), kTileThreads, smem, s>>>(d, P.packed, PL, P);
-  ALTO_LAUNCH_CHECK("alto_mttkrp(planned2)");
-  return ALTO_OK;
-}
-
-template <int W, typename V, typename O>
-int try_planned2(const DevLayout& d, const StreamParams& P, const Plan2& PL, cudaStream_t s) {
-  if (!P.packed || !PL.plan) return ALTO_EUNSUPPORTED;
-  long long maxdim = 0;
-  for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
-  if (maxdim * P.rank * static_cast<long long>(sizeof(V)) / 16 >= 0x80000000ll) return ALTO_EUNSUPPORTED;
-  for (int n = 0; n < d.order; ++n)
-    if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
-  if (P.rank == 16) {
-    if (d.order == 3) return launch_planned2<W, V, O, 3, 16>(d, P, PL, s);
-    if (d.order == 4) return launch_planned2<W, V, O, 4, 16>(d, P, PL, s);
-    if (d.order == 5) return launch_planned2<W, V, O, 5, 16>(d, P, PL, s);
-  }
-  if (P.rank == 32) {
-    if (d.order == 3) return launch_planned2<W, V, O, 3, 32>(d, P, PL, s);
-    if (d.order == 4) return launch_planned2<W, V, O, 4, 32>(d, P, PL, s);
-    if (d.order == 5) return launch_planned2<W, V, O, 5, 32>(d, P, PL, s);
   }
   return ALTO_EUNSUPPORTED;
 }

@@ -108,6 +108,30 @@ inline MsFields ms_fields(const DevLayout& d, int mode) {
   return f;
 }
 
+// Delta stream layout (ALTO_MS_DELTA, 128-bit layouts): one 64-bit word per
+// element holding the input-mode coordinates (ascending, no field straddling
+// bit 63) and, in place of the output coordinate, the row increment from the
+// previous element of the same lane group (its base row is stored per group,
+// alto_mode_stream base_rows); bit 63 = hot-row flag.  `ok` needs at least 8
+// increment bits.
+inline MsFields ms_fields_delta(const DevLayout& d, int mode) {
+  MsFields f{};
+  int cur = 0;
+  for (int n = 0; n < d.order; ++n) {
+    if (n == mode) continue;
+    f.word[n] = 0;
+    f.sh[n] = cur;
+    f.mask[n] = d.bits[n] >= 32 ? 0xffffffffu : ((1u << d.bits[n]) - 1u);
+    cur += d.bits[n];
+  }
+  const int db = std::min(31, 63 - cur);
+  f.word[mode] = 0;
+  f.sh[mode] = cur;
+  f.mask[mode] = db >= 1 ? ((1u << db) - 1u) : 0u;
+  f.ok = db >= 8;
+  return f;
+}
+
 // One field selector held in registers (hoisted out of the element loops).
 struct FSel {
   unsigned sh, mask;
@@ -138,10 +162,10 @@ struct MStream {
   MsFields f;
   int rr;                // round-robin slices: group s takes sorted positions s, s+8, ...
   VIn vin[ALTO_MAX_ORDER];  // gathered inputs when input modes are paired (P.n_pairs > 0)
+  const int* base;       // delta stream: row of every lane group's first element (ntiles x 8)
 };
 
-template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, bool COOP = false,
-          bool XCH_SHFL = false, bool XKEY = false, int NV = N - 1>
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, int NV = N - 1, bool DELTA = false>
 __global__ void __launch_bounds__(kTileThreads, MINB)
 mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStream S,
                const __grid_constant__ StreamParams P) {
@@ -154,11 +178,9 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
   constexpr bool PAIR = NV < N - 1;
   constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
   constexpr unsigned HOTF = 0x80000000u;
-  static_assert(!COOP || (U >= 1 && U <= G), "one decoding lane per element of a block");
+  static_assert(U >= 1 && U <= G, "one decoding lane per element of a block");
   constexpr int VW = static_cast<int>(sizeof(V) / 4);
   constexpr int NWREC = (NIN + 1 + VW + 3) & ~3;  // record words (16-byte multiple)
-  __shared__ __align__(16) unsigned s_rec_all[COOP && !XCH_SHFL ? (kTileThreads / 32) * U * GPW * NWREC : 4];
-  unsigned* s_rec = s_rec_all + (COOP && !XCH_SHFL ? (threadIdx.x >> 5) * U * GPW * NWREC : 0);
   const int mode = P.mode;
   const int T = S.tile;
   const int CH = T / kMsSlices;
@@ -254,58 +276,10 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
       auto target = [&](const Key<W>& k) {
         return ms_field<W>(k, fout) | (static_cast<unsigned>(k.w[W - 1] >> 32) & hotmask);
       };
-      if constexpr (!COOP) {
-        // Broadcast loads: the G lanes of a group load the same key/value
-        // (the warp's 8 slices at step j are 8 consecutive keys: one request)
-        // and decode it redundantly with two shifts per field.  The next U
-        // elements' keys/values are loaded while the current U elements'
-        // factor rows are gathered.
-        auto run = [&](auto full_tag) {
-          constexpr bool FULL = decltype(full_tag)::value;
-          Key<W> nk[U];
-          V nv[U];
-          const uint64_t* kq = kp;
-          const V* vq = vp;
-          auto prefetch = [&](int jb) {
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-              if (FULL || jb + u < len) {
-                nk[u] = load_key_stream<W>(kq, static_cast<long long>(u) * kMsSlices, pol);
-                nv[u] = load_val_stream<V>(vq + u * kMsSlices, pol);
-              }
-            kq += U * kMsSlices * W;
-            vq += U * kMsSlices;
-          };
-          prefetch(0);
-#pragma unroll 1
-          for (int j0 = 0; j0 < jmax; j0 += U) {
-            Key<W> kk[U];
-            V vv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) { kk[u] = nk[u]; vv[u] = nv[u]; }
-            if (FULL ? j0 + U < jmax : true) prefetch(j0 + U);
-            V4<F> g[U][NIN];
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-              if (FULL || j0 + u < len)
-#pragma unroll
-                for (int k = 0; k < NIN; ++k) g[u][k] = gather_off<F>(fin_lane[k], voff(kk[u], k));
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-              if (FULL || j0 + u < len) consume(target(kk[u]), vv[u], g[u]);
-          }
-        };
-        if (cnt == T && CH % U == 0)
-          run(std::integral_constant<bool, true>{});
-        else
-          run(std::integral_constant<bool, false>{});
-      } else {
+      {
         // Cooperative decode: lane gl < U of a group loads and decodes element
         // j0+gl of the group's slice; the U decoded records {input row byte
-        // offsets, target, value} are broadcast within the group by shuffles
-        // (XCH_SHFL, default) or through a per-warp shared-memory block (one
-        // STS.128 per decoding lane, one broadcast LDS.128 per group and
-        // element: half the L1 wavefronts, but measured slower on cfg2).
+        // offsets, target, value} are broadcast within the group by shuffles.
         Key<W> nk{};
         V nv = V(0);
         auto prefetch = [&](int jb) {
@@ -317,6 +291,9 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
         };
         prefetch(0);
         const int gbase = lane & ~(G - 1);
+        // delta stream: running row of the group (its first element's row)
+        unsigned carry = 0;
+        if constexpr (DELTA) carry = len > 0 ? static_cast<unsigned>(__ldg(S.base + t * kMsSlices + s)) : 0u;
 #pragma unroll 1
         for (int j0 = 0; j0 < jmax; j0 += U) {
           const Key<W> kk = nk;
@@ -325,30 +302,26 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
           unsigned moff[NIN];
 #pragma unroll
           for (int k = 0; k < NIN; ++k) moff[k] = voff(kk, k);
-          const unsigned mtg = (gl < U && j0 + gl < len) ? target(kk) : 0xffffffffu;
+          unsigned mtg;
+          if constexpr (DELTA) {
+            // rows = carry + inclusive prefix of the U decoded increments (lanes gl < U)
+            const bool ok = gl < U && j0 + gl < len;
+            unsigned dlt = ok ? ms_field<W>(kk, fout) : 0u;
+#pragma unroll
+            for (int o = 1; o < U; o <<= 1) {
+              const unsigned y = __shfl_up_sync(0xffffffffu, dlt, o, G);
+              if (gl >= o) dlt += y;
+            }
+            const unsigned row = carry + dlt;
+            carry = __shfl_sync(0xffffffffu, row, gbase + U - 1);
+            mtg = ok ? (row | (static_cast<unsigned>(kk.w[W - 1] >> 32) & hotmask)) : 0xffffffffu;
+          } else {
+            mtg = (gl < U && j0 + gl < len) ? target(kk) : 0xffffffffu;
+          }
           V4<F> g[U][NIN];
           unsigned tg[U];
           V vu[U];
-          if constexpr (XCH_SHFL && XKEY) {
-            // shuffle the raw key (2W words) and value; every lane decodes the
-            // fields itself (fewer shuffles than offsets + target + value
-            // when 2W < N, but measured slower on cfg2; A/B variant)
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              Key<W> ku;
-#pragma unroll
-              for (int q = 0; q < W; ++q) {
-                const unsigned lo = __shfl_sync(0xffffffffu, static_cast<unsigned>(kk.w[q]), gbase + u);
-                const unsigned hi = __shfl_sync(0xffffffffu, static_cast<unsigned>(kk.w[q] >> 32), gbase + u);
-                ku.w[q] = (static_cast<uint64_t>(hi) << 32) | lo;
-              }
-              vu[u] = __shfl_sync(0xffffffffu, vv, gbase + u);
-              tg[u] = j0 + u < len ? target(ku) : 0xffffffffu;
-#pragma unroll
-              for (int k = 0; k < NIN; ++k)
-                if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], voff(ku, k));
-            }
-          } else if constexpr (XCH_SHFL) {
+          {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               tg[u] = __shfl_sync(0xffffffffu, mtg, gbase + u);
@@ -358,48 +331,6 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
                 const unsigned off = __shfl_sync(0xffffffffu, moff[k], gbase + u);
                 if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], off);
               }
-            }
-          } else {
-            __syncwarp();  // previous block's records are consumed
-            if (gl < U) {
-              unsigned w[NWREC];
-#pragma unroll
-              for (int k = 0; k < NIN; ++k) w[k] = moff[k];
-              w[NIN] = mtg;
-              if constexpr (sizeof(V) == 4) {
-                w[NIN + 1] = __float_as_uint(vv);
-              } else {
-                const unsigned long long b = __double_as_longlong(vv);
-                w[NIN + 1] = static_cast<unsigned>(b);
-                w[NIN + 2] = static_cast<unsigned>(b >> 32);
-              }
-#pragma unroll
-              for (int q = NIN + 1 + VW; q < NWREC; ++q) w[q] = 0u;
-              unsigned* dst = s_rec + (gl * GPW + grp) * NWREC;
-#pragma unroll
-              for (int q = 0; q < NWREC; q += 4)
-                *reinterpret_cast<uint4*>(dst + q) = make_uint4(w[q], w[q + 1], w[q + 2], w[q + 3]);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              unsigned w[NWREC];
-              const unsigned* src = s_rec + (u * GPW + grp) * NWREC;
-#pragma unroll
-              for (int q = 0; q < NWREC; q += 4) {
-                const uint4 t4 = *reinterpret_cast<const uint4*>(src + q);
-                w[q] = t4.x; w[q + 1] = t4.y; w[q + 2] = t4.z; w[q + 3] = t4.w;
-              }
-              tg[u] = w[NIN];
-              if constexpr (sizeof(V) == 4) {
-                vu[u] = __uint_as_float(w[NIN + 1]);
-              } else {
-                vu[u] = __longlong_as_double(static_cast<long long>(
-                    (static_cast<unsigned long long>(w[NIN + 2]) << 32) | w[NIN + 1]));
-              }
-#pragma unroll
-              for (int k = 0; k < NIN; ++k)
-                if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], w[k]);
             }
           }
 #pragma unroll
@@ -413,17 +344,17 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
 }
 
 // Elements in flight per group: ~UREG registers of gathered factor data per
-// lane (cooperative decode: U <= G, one decoding lane per element).
-template <int N, int R, typename V, int UREG, bool COOP>
+// lane, at most one decoding lane per element (U <= G).
+template <int N, int R, typename V, int UREG>
 constexpr int ms_u() {
   constexpr int ub = std::max(1, UREG / ((N - 1) * 4 * static_cast<int>(sizeof(V) / 4)));
-  return COOP ? std::min(R / 4, ub) : ub;
+  return std::min(R / 4, ub);
 }
 
-template <int W, typename V, typename O, int N, int R, bool COOP = true, int MINB = 3,
-          int U = ms_u<N, R, V, (COOP ? 32 : 16), COOP>(), bool XCH_SHFL = true, bool XKEY = false, int NV = N - 1>
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = ms_u<N, R, V, 32>(), int NV = N - 1,
+          bool DELTA = false>
 int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, cudaStream_t s) {
-  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, COOP, XCH_SHFL, XKEY, NV>;
+  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, NV, DELTA>;
   static int cached_bps = 0;
   if (!cached_bps) {
     int b = 1;
@@ -438,17 +369,9 @@ int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, 
   return ALTO_OK;
 }
 
-// Returns ALTO_EUNSUPPORTED (without launching) when the shape is not covered.
-template <int W, typename V, typename O>
-int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
-  if (!P.mkeys || !P.mvals || P.mtile <= 0) return ALTO_EUNSUPPORTED;
-  long long maxdim = 0;
-  for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
-  if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
-  for (int n = 0; n < d.order; ++n)
-    if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
-  MStream S{P.mkeys, P.mvals, P.mtile, ms_fields(d, P.mode), P.mrr, {}};
-  if (!S.f.ok) return ALTO_EUNSUPPORTED;
+// Dispatch of one stream layout (DELTA: one-word delta keys, W = 1).
+template <int W, typename V, typename O, bool DELTA>
+int mstream_dispatch(const DevLayout& d, MStream S, const StreamParams& P, cudaStream_t s) {
   if (P.n_pairs > 0) {
     // paired input modes (alto_krp_pair tables): float32 data, rank 16, orders 4-5
     if constexpr (sizeof(V) == 4 && !std::is_same<O, long long>::value) {
@@ -465,42 +388,54 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
       }
       for (int n = 0; n < d.order; ++n)
         if (!((used >> n) & 1u)) S.vin[nv++] = VIn{P.factors[n], n, -1, 1u};
-      if (d.order == 4 && nv == 2) return launch_mstream<W, V, O, 4, 16, true, 3, ms_u<3, 16, V, 32, true>(), true, false, 2>(d, S, P, s);
-      if (d.order == 5 && nv == 3) return launch_mstream<W, V, O, 5, 16, true, 3, ms_u<4, 16, V, 32, true>(), true, false, 3>(d, S, P, s);
-      if (d.order == 5 && nv == 2) return launch_mstream<W, V, O, 5, 16, true, 3, ms_u<3, 16, V, 32, true>(), true, false, 2>(d, S, P, s);
+      if (d.order == 4 && nv == 2)
+        return launch_mstream<W, V, O, 4, 16, 3, ms_u<3, 16, V, 32>(), 2, DELTA>(d, S, P, s);
+      if (d.order == 5 && nv == 3)
+        return launch_mstream<W, V, O, 5, 16, 3, ms_u<4, 16, V, 32>(), 3, DELTA>(d, S, P, s);
+      if (d.order == 5 && nv == 2)
+        return launch_mstream<W, V, O, 5, 16, 3, ms_u<3, 16, V, 32>(), 2, DELTA>(d, S, P, s);
     }
     return ALTO_EUNSUPPORTED;
   }
-  if constexpr (W == 1 && sizeof(V) == 4 && sizeof(O) == 4) {
-    // tuning variants for the cfg2 shape (A/B only)
-    if (d.order == 3 && P.rank == 16) {
-      const int f = P.flags & (ALTO_STREAM_MS_COOP | ALTO_STREAM_TUNE_MINB2 | ALTO_STREAM_TUNE_U4);
-      // measured on cfg2 (ms/mode): cooperative U=4 0.61-0.63 (default), U=3
-      // 0.67-0.69, broadcast 0.70-0.72, cooperative at 2 CTAs/SM 0.75-0.79,
-      // broadcast U=4 at 2 CTAs/SM 0.73-0.77
-      if (f == ALTO_STREAM_MS_COOP) return launch_mstream<W, V, O, 3, 16, false>(d, S, P, s);
-      // (4 CTAs/SM at 64 registers with U=3 / U=2: 0.64-0.66 / 0.66-0.68 ms; a
-      // two-stage software pipeline of U=2 / U=3 blocks: 0.65-0.68 / 0.86-0.88
-      // ms — both dropped)
-      // shared-memory record exchange: 0.66-0.68 ms (fewer wavefronts, but
-      // the two __syncwarp per block cost more than the shuffles)
-      if (f == ALTO_STREAM_TUNE_U4) return launch_mstream<W, V, O, 3, 16, true, 3, 4, false>(d, S, P, s);
-      // shuffling the raw key + value (3 shuffles, every lane decodes) instead
-      // of offsets + target + value (4): 0.69-0.73 ms (decode costs more)
-      if (f == ALTO_STREAM_TUNE_MINB2) return launch_mstream<W, V, O, 3, 16, true, 3, 4, true, true>(d, S, P, s);
-    }
-  }
+  // (measured and dropped on cfg2, ms/mode: broadcast key loads 0.70-0.72,
+  // 4 CTAs/SM 0.64-0.68, a two-stage pipeline 0.65-0.88, a shared-memory
+  // record exchange 0.66-0.68, raw-key shuffles 0.69-0.73 — against 0.45-0.46
+  // for this cooperative-decode + shuffle kernel with round-robin groups)
   if (P.rank == 16) {
-    if (d.order == 3) return launch_mstream<W, V, O, 3, 16>(d, S, P, s);
-    if (d.order == 4) return launch_mstream<W, V, O, 4, 16>(d, S, P, s);
-    if (d.order == 5) return launch_mstream<W, V, O, 5, 16>(d, S, P, s);
+    if (d.order == 3) return launch_mstream<W, V, O, 3, 16, 3, ms_u<3, 16, V, 32>(), 2, DELTA>(d, S, P, s);
+    if (d.order == 4) return launch_mstream<W, V, O, 4, 16, 3, ms_u<4, 16, V, 32>(), 3, DELTA>(d, S, P, s);
+    if (d.order == 5) return launch_mstream<W, V, O, 5, 16, 3, ms_u<5, 16, V, 32>(), 4, DELTA>(d, S, P, s);
   }
   if (P.rank == 32) {
-    if (d.order == 3) return launch_mstream<W, V, O, 3, 32>(d, S, P, s);
-    if (d.order == 4) return launch_mstream<W, V, O, 4, 32>(d, S, P, s);
-    if (d.order == 5) return launch_mstream<W, V, O, 5, 32>(d, S, P, s);
+    if (d.order == 3) return launch_mstream<W, V, O, 3, 32, 3, ms_u<3, 32, V, 32>(), 2, DELTA>(d, S, P, s);
+    if (d.order == 4) return launch_mstream<W, V, O, 4, 32, 3, ms_u<4, 32, V, 32>(), 3, DELTA>(d, S, P, s);
+    if (d.order == 5) return launch_mstream<W, V, O, 5, 32, 3, ms_u<5, 32, V, 32>(), 4, DELTA>(d, S, P, s);
   }
   return ALTO_EUNSUPPORTED;
+}
+
+// Returns ALTO_EUNSUPPORTED (without launching) when the shape is not covered.
+template <int W, typename V, typename O>
+int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s) {
+  if (!P.mkeys || !P.mvals || P.mtile <= 0) return ALTO_EUNSUPPORTED;
+  long long maxdim = 0;
+  for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
+  if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
+  for (int n = 0; n < d.order; ++n)
+    if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
+  if (P.mbase) {
+    // delta stream: one key word whatever the layout width (ALTO_MS_DELTA)
+    if constexpr (W != 1) {
+      return try_mstream<1, V, O>(d, P, s);
+    } else {
+      const MStream S{P.mkeys, P.mvals, P.mtile, ms_fields_delta(d, P.mode), P.mrr, {}, P.mbase};
+      if (!S.f.ok) return ALTO_EUNSUPPORTED;
+      return mstream_dispatch<1, V, O, true>(d, S, P, s);
+    }
+  }
+  const MStream S{P.mkeys, P.mvals, P.mtile, ms_fields(d, P.mode), P.mrr, {}, nullptr};
+  if (!S.f.ok) return ALTO_EUNSUPPORTED;
+  return mstream_dispatch<W, V, O, false>(d, S, P, s);
 }
 
 // out[row(s)] += sum of the row's copies (float64, fixed order), copies re-zeroed.

@@ -117,7 +117,9 @@ __global__ void mstream_scatter_kernel(const __grid_constant__ DevLayout L, cons
                                        const uint64_t* __restrict__ packed, const V* __restrict__ vals,
                                        const unsigned* __restrict__ idx, long long m, int mode, int tile,
                                        int round_robin, const int* __restrict__ hot_slot,
-                                       uint64_t* __restrict__ skeys, V* __restrict__ svals) {
+                                       uint64_t* __restrict__ skeys, V* __restrict__ svals,
+                                       const uint64_t* __restrict__ srows, int* __restrict__ base_rows,
+                                       int* __restrict__ overflow) {
   const int ch = tile / kMsSlices;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < m; q += stride) {
@@ -129,12 +131,38 @@ __global__ void mstream_scatter_kernel(const __grid_constant__ DevLayout L, cons
     // (consecutive elements in one instruction), stored in sorted order
     const long long dst = round_robin ? q : t * tile + static_cast<long long>(p % ch) * kMsSlices + p / ch;
     const Key<W> k = load_key<W>(packed, src);
+    const unsigned row = packed_field32<W>(k, L.pack_off[mode], L.bits[mode]);
+    const bool hot = hot_slot && hot_slot[row] >= 0;
+    if (base_rows) {
+      // delta stream: inputs + increment from the group's previous element
+      // (srows = the sorted row of every position, so its neighbour is known)
+      const int gs = round_robin ? (p % kMsSlices) : (p / ch);
+      const int gj = round_robin ? (p / kMsSlices) : (p % ch);
+      const long long prev = round_robin ? q - kMsSlices : q - 1;
+      uint64_t w = 0;
+      for (int n = 0; n < L.order; ++n) {
+        if (n == mode) continue;
+        w |= static_cast<uint64_t>(packed_field32<W>(k, L.pack_off[n], L.bits[n])) << F.sh[n];
+      }
+      unsigned dlt = 0;
+      if (gj == 0) {
+        base_rows[t * kMsSlices + gs] = static_cast<int>(row);
+      } else {
+        dlt = row - static_cast<unsigned>(srows[prev]);
+        if (dlt > F.mask[mode]) atomicExch(overflow, 1);
+      }
+      w |= static_cast<uint64_t>(dlt & F.mask[mode]) << F.sh[mode];
+      if (hot) w |= 1ull << 63;
+      skeys[dst] = w;
+      svals[dst] = vals[src];
+      continue;
+    }
     Key<W> o{};
     for (int n = 0; n < L.order; ++n) {
       const uint64_t c = packed_field32<W>(k, L.pack_off[n], L.bits[n]);
       o.w[W == 1 ? 0 : F.word[n]] |= c << F.sh[n];
     }
-    if (hot_slot && hot_slot[packed_field32<W>(k, L.pack_off[mode], L.bits[mode])] >= 0) o.w[W - 1] |= 1ull << 63;
+    if (hot) o.w[W - 1] |= 1ull << 63;
     store_key<W>(skeys, dst, o);
     svals[dst] = vals[src];
   }
@@ -191,7 +219,8 @@ size_t alto_mode_stream_workspace_bytes(int64_t m) {
 
 int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,
                      int64_t m, int32_t mode, int32_t tile, int32_t flags, const int32_t* hot_slot, uint64_t* skeys,
-                     void* svals, void* ws, size_t ws_bytes, void* stream) {
+                     void* svals, int32_t* base_rows, int32_t* d_overflow, void* ws, size_t ws_bytes,
+                     void* stream) {
   ALTO_REQUIRE(lay && lay->order >= 1 && lay->order <= ALTO_MAX_ORDER, "bad layout");
   ALTO_REQUIRE(mode >= 0 && mode < lay->order, "mode out of range");
   ALTO_REQUIRE(lay->bits[mode] <= 31, "mode stream needs mode extents below 2^31");
@@ -199,11 +228,15 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
   ALTO_REQUIRE(tile >= 128 && tile % 128 == 0, "tile must be a positive multiple of 128");
   ALTO_REQUIRE(m >= 0 && m < (1ll << 32) - 1, "mode stream supports fewer than 2^32 elements");
   const DevLayout d = make_dev_layout(lay);
-  const MsFields F = ms_fields(d, mode);
+  const bool delta = (flags & ALTO_MS_DELTA) != 0;
+  ALTO_REQUIRE(!delta || ((flags & ALTO_MS_ROW_MAJOR) && base_rows && d_overflow),
+               "delta stream needs row-major order, base_rows and d_overflow");
+  const MsFields F = delta ? ms_fields_delta(d, mode) : ms_fields(d, mode);
   if (!F.ok) {
     set_error("mode stream: the mode's field layout does not fit the key width");
     return ALTO_EUNSUPPORTED;
   }
+  const int sw = delta ? 1 : d.n_words;  // stream key words
   const long long ntiles = (m + tile - 1) / tile;
   const int row_major = (flags & ALTO_MS_ROW_MAJOR) ? 1 : 0;
   int tbits = 0;
@@ -212,9 +245,9 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
   cudaStream_t s = as_stream(stream);
   const size_t vb = value_dtype == ALTO_F32 ? 4 : 8;
   const size_t padded = static_cast<size_t>(ntiles) * tile;
+  if (delta) ALTO_CUDA_TRY(cudaMemsetAsync(d_overflow, 0, sizeof(int32_t), s));
   if (padded > static_cast<size_t>(m)) {
-    ALTO_CUDA_TRY(cudaMemsetAsync(skeys + static_cast<size_t>(m) * d.n_words, 0,
-                                  (padded - m) * 8 * d.n_words, s));
+    ALTO_CUDA_TRY(cudaMemsetAsync(skeys + static_cast<size_t>(m) * sw, 0, (padded - m) * 8 * sw, s));
     ALTO_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(svals) + m * vb, 0, (padded - m) * vb, s));
   }
   if (m <= 0) return ALTO_OK;
@@ -237,7 +270,8 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
 #define ALTO_MS_SCATTER(WW, VT)                                                                              \
   mstream_scatter_kernel<WW, VT><<<grid, 256, 0, s>>>(d, F, packed, static_cast<const VT*>(values), idx, m, mode, \
                                                       tile, (flags & ALTO_MS_ROUND_ROBIN) ? 1 : 0, hs, skeys,    \
-                                                      static_cast<VT*>(svals))
+                                                      static_cast<VT*>(svals), delta ? ckey : nullptr,           \
+                                                      delta ? base_rows : nullptr, d_overflow)
   if (d.n_words == 1) {
     if (vb == 4) ALTO_MS_SCATTER(1, float); else ALTO_MS_SCATTER(1, double);
   } else {
@@ -253,115 +287,6 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
 // ---- plan 2: per-mode 64-bit plan words and hot-input row selection ----------
 namespace alto {
 
-struct SlotMaps {
-  const int* in_slot[kMaxCacheModes];  // per input mode k (mode order, output mode skipped)
-  const int* hot_out;                   // hot output slot per row (-1 = not hot), or null
-};
-
-template <int W>
-__global__ void stream_plan_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ packed,
-                                   long long m, int mode, const __grid_constant__ SlotMaps S,
-                                   unsigned long long* __restrict__ plan) {
-  __shared__ int s_bins[kTileThreads / 32][kFastBins];
-  constexpr int EPL = kPlanTile / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int* bin = s_bins[warp];
-  const long long nsub = (m + kPlanTile - 1) / kPlanTile;
-  const long long nwarps = static_cast<long long>(gridDim.x) * (kTileThreads / 32);
-  const unsigned ltm = (1u << lane) - 1u;
-  const int N = L.order;
-  for (long long sub = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp; sub < nsub; sub += nwarps) {
-    const long long e0 = sub * kPlanTile;
-    const int cnt = static_cast<int>(min(static_cast<long long>(kPlanTile), m - e0));
-    int row[EPL];
-    unsigned long long word[EPL];
-    int lo = INT_MAX, hi = INT_MIN;
-#pragma unroll
-    for (int k = 0; k < EPL; ++k) {
-      const int e = lane + 32 * k;
-      row[k] = -1;
-      word[k] = 0;
-      if (e < cnt) {
-        const Key<W> key = load_key<W>(packed, e0 + e);
-        unsigned long long w = 0;
-        int q = 0;
-        for (int n = 0; n < N; ++n) {
-          const int c = static_cast<int>(packed_field32<W>(key, L.pack_off[n], L.bits[n]));
-          if (n == mode) {
-            row[k] = c;
-            if (S.hot_out) {
-              const int hs = S.hot_out[c];
-              if (hs >= 0) w |= static_cast<unsigned long long>((hs + 1) & 0xffff) << 32;
-            }
-          } else {
-            unsigned h = 0xffu;
-            if (q < kMaxCacheModes && S.in_slot[q]) {
-              const int sl = S.in_slot[q][c];
-              if (sl >= 0 && sl < 255) h = static_cast<unsigned>(sl);
-            }
-            if (q < kMaxCacheModes) w |= static_cast<unsigned long long>(h) << (8 + 8 * q);
-            ++q;
-          }
-        }
-        word[k] = w;
-        lo = min(lo, row[k]);
-        hi = max(hi, row[k]);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    const int span = hi - lo + 1;
-    if (span > kFastBins) {
-#pragma unroll
-      for (int k = 0; k < EPL; ++k)
-        if (row[k] >= 0) plan[e0 + lane + 32 * k] = word[k] | static_cast<unsigned long long>(lane + 32 * k);
-      continue;
-    }
-    for (int i = lane; i < span; i += 32) bin[i] = 0;
-    __syncwarp();
-    unsigned peers[EPL];
-#pragma unroll
-    for (int k = 0; k < EPL; ++k) {
-      const bool ok = row[k] >= 0;
-      peers[k] = __match_any_sync(0xffffffffu, ok ? row[k] : -1 - lane);
-      if (ok && (peers[k] & ltm) == 0) bin[row[k] - lo] += __popc(peers[k]);
-      __syncwarp();
-    }
-    int carry = 0;
-    for (int base = 0; base < span; base += 32) {
-      const int i = base + lane;
-      const int v = i < span ? bin[i] : 0;
-      int x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (i < span) bin[i] = carry + x - v;
-      carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < EPL; ++k) {
-      const bool ok = row[k] >= 0;
-      const int leader = __ffs(peers[k]) - 1;
-      int b = 0;
-      if (ok && leader == lane) {
-        b = bin[row[k] - lo];
-        bin[row[k] - lo] = b + __popc(peers[k]);
-      }
-      b = __shfl_sync(0xffffffffu, b, leader);
-      if (ok) plan[e0 + lane + 32 * k] = word[k] | static_cast<unsigned long long>(b + __popc(peers[k] & ltm));
-      __syncwarp();
-    }
-  }
-}
-
-// keys[r] = (count << 32) | (0xffffffff - r) so an ascending sort puts the
-// highest counts last (ties: lower row first).
 __global__ void topk_keys_kernel(const long long* __restrict__ row_ptr, long long dim, uint64_t* __restrict__ keys) {
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < dim; r += stride) {
@@ -402,24 +327,6 @@ size_t alto_topk_rows_workspace_bytes(int64_t dim) {
   return ((static_cast<size_t>(dim) * 8 + 255) & ~size_t(255)) + alto_sort_workspace_bytes(dim, 1, 0);
 }
 
-int alto_topk_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int32_t* rows, int32_t* slot_map, void* ws,
-                   size_t ws_bytes, void* stream) {
-  ALTO_REQUIRE(dim >= 1 && dim <= INT_MAX, "topk needs 1 <= dim < 2^31");
-  ALTO_REQUIRE(k >= 1 && k <= 255, "topk k must be in [1, 255]");
-  ALTO_REQUIRE(ws && ws_bytes >= alto_topk_rows_workspace_bytes(dim), "topk workspace too small");
-  cudaStream_t s = as_stream(stream);
-  auto* keys = static_cast<uint64_t*>(ws);
-  const size_t a = (static_cast<size_t>(dim) * 8 + 255) & ~size_t(255);
-  topk_keys_kernel<<<grid_for(dim, 256), 256, 0, s>>>(reinterpret_cast<const long long*>(row_ptr), dim, keys);
-  fill_i32<<<grid_for(dim, 256), 256, 0, s>>>(slot_map, dim, -1);
-  ALTO_LAUNCH_CHECK("alto_topk_rows");
-  const int st = alto_sort_pairs(keys, nullptr, dim, 1, 0, 64, static_cast<char*>(ws) + a, ws_bytes - a, stream);
-  if (st) return st;
-  topk_finish_kernel<<<1, 256, 0, s>>>(keys, dim, k, 0ull, rows, slot_map, nullptr);
-  ALTO_LAUNCH_CHECK("alto_topk_rows/finish");
-  return ALTO_OK;
-}
-
 int alto_hot_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int64_t min_count, int32_t* rows,
                   int32_t* slot_map, int32_t* d_count, void* ws, size_t ws_bytes, void* stream) {
   ALTO_REQUIRE(dim >= 1 && dim <= INT_MAX, "hot rows need 1 <= dim < 2^31");
@@ -440,31 +347,5 @@ int alto_hot_rows(const int64_t* row_ptr, int64_t dim, int32_t k, int64_t min_co
   return ALTO_OK;
 }
 
-int alto_stream_plan(const alto_layout* lay, const uint64_t* packed, int64_t m, int32_t mode,
-                     const int32_t* const* in_slot_maps_host, const int32_t* hot_out_slot, uint64_t* plan,
-                     void* stream) {
-  ALTO_REQUIRE(lay && mode >= 0 && mode < lay->order, "mode out of range");
-  for (int n = 0; n < lay->order; ++n) ALTO_REQUIRE(lay->bits[n] <= 31, "stream plan needs extents below 2^31");
-  if (m <= 0) return ALTO_OK;
-  const DevLayout d = make_dev_layout(lay);
-  SlotMaps S{};
-  int q = 0;
-  for (int n = 0; n < lay->order; ++n) {
-    if (n == mode) continue;
-    if (q < kMaxCacheModes) S.in_slot[q] = in_slot_maps_host ? in_slot_maps_host[n] : nullptr;
-    ++q;
-  }
-  S.hot_out = hot_out_slot;
-  cudaStream_t s = as_stream(stream);
-  const long long nsub = (m + kPlanTile - 1) / kPlanTile;
-  const int grid = grid_for(nsub, kTileThreads / 32, kSMs * 8);
-  auto* pl = reinterpret_cast<unsigned long long*>(plan);
-  if (d.n_words == 1)
-    stream_plan_kernel<1><<<grid, kTileThreads, 0, s>>>(d, packed, m, mode, S, pl);
-  else
-    stream_plan_kernel<2><<<grid, kTileThreads, 0, s>>>(d, packed, m, mode, S, pl);
-  ALTO_LAUNCH_CHECK("alto_stream_plan");
-  return ALTO_OK;
-}
 
 }  // extern "C"

@@ -11,7 +11,7 @@
 //   2. exclusive scan of counts (digit-major, so the scan yields the global
 //      destination of (digit, tile) directly)
 //   3. radix_scatter: stable in-tile ranking.  Each warp owns a contiguous
-//      512-key slice of the 4096-key tile, visited in index order
+//      256-key slice of the 2048-key tile, visited in index order
 //      (round j, lane l); __match_any_sync groups equal digits, the group's
 //      lower lanes give the rank, per-warp running digit counters carry the
 //      rank across rounds, and a per-digit exclusive scan over warps orders
@@ -27,10 +27,10 @@
 namespace alto {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kWarpSlice = kSortTile / kSortWarps;     // 512 keys per warp
+constexpr int kWarpSlice = kSortTile / kSortWarps;     // 256 keys per warp
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanChunk = kScanThreads * kScanItems;  // 4096 counters
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
   const long long base = tile * kSortTile + static_cast<long long>(warp) * kWarpSlice;
   const unsigned lt_mask = (1u << lane) - 1u;
   // Ranking pass: only the key word holding the digit is read; each item
-  // keeps (rank << 8 | digit) in one register (ranks < 4096), so the kernel
+  // keeps (rank << 8 | digit) in one register (ranks < 2048), so the kernel
   // stays small enough for several CTAs per SM; keys and payload are re-read
   // (L2 hits) in the placement pass below.
   const int dw = shift >> 6;

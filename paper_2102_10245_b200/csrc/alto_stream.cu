@@ -168,6 +168,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.mvals = a->mvals;
   P.mtile = a->mtile;
   P.mrr = a->mrr;
+  P.mbase = a->mkeys ? a->mbase : nullptr;
   P.n_pairs = (a->mkeys && a->out_dtype != ALTO_I64) ? std::max(0, std::min(a->n_pairs, 2)) : 0;
   ALTO_REQUIRE(a->n_pairs <= 2, "at most 2 paired input modes");
   for (int i = 0; i < 2; ++i) {
@@ -179,17 +180,6 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
                "mode stream needs values and a tile that is a multiple of 128");
   ALTO_REQUIRE(!a->mkeys || a->n_hot <= 0 || a->hot_base, "mode-stream hot plan needs hot_base");
   ALTO_REQUIRE(!a->mkeys || a->rank <= 32, "the mode-stream hot-row reduction supports ranks up to 32");
-  Plan2 pl2{};
-  P.plan2 = nullptr;
-  if (a->plan) {
-    pl2.plan = reinterpret_cast<const unsigned long long*>(a->plan);
-    for (int k = 0; k < kMaxCacheModes; ++k) pl2.cache_rows[k] = a->cache_rows[k];
-    pl2.cache_k = a->cache_k;
-    pl2.cache_modes = a->cache_k > 0 ? std::min(a->cache_modes, kMaxCacheModes) : 0;
-    for (int k = 0; k < pl2.cache_modes; ++k) ALTO_REQUIRE(pl2.cache_rows[k] != nullptr, "cache rows missing");
-    ALTO_REQUIRE(pl2.cache_k >= 0 && pl2.cache_k <= 255, "cache_k must be in [0, 255]");
-    P.plan2 = &pl2;
-  }
   const auto* tab = static_cast<const uint64_t*>(a->d_tables);
   const bool o32 = a->out_dtype == ALTO_F32;
   if (a->out_dtype == ALTO_I64) {
@@ -218,6 +208,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
                                  : fast_w1_f64(d, tab, P, a->value_dtype, a->factor_dtype, s))
                           : (o32 ? fast_w2_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
                                  : fast_w2_f64(d, tab, P, a->value_dtype, a->factor_dtype, s));
+  if (st == ALTO_EUNSUPPORTED && a->mkeys) return st;  // mode-stream arguments (hot plan) mean nothing to the generic kernel
   if (st == ALTO_EUNSUPPORTED)
     st = d.n_words == 1 ? (o32 ? stream_w1_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
                                  : stream_w1_f64(d, tab, P, a->value_dtype, a->factor_dtype, s))

@@ -43,7 +43,6 @@ constexpr int kSortBins = 2048;
 constexpr int kEPT = 4;  // elements per thread in phase A -> tile <= 1024
 constexpr int kRecPad = 4 * kTileThreads;  // words of swizzle headroom (4 per phase-B chunk)
 
-struct Plan2;
 struct StreamParams {
   const uint64_t* keys;
   const void* values;
@@ -61,11 +60,11 @@ struct StreamParams {
   int flags;
   const uint64_t* packed;     // mode-contiguous keys (optional, alto_pack_keys)
   const unsigned char* pos;   // per-mode sub-tile slots (optional, alto_subtile_order)
-  const Plan2* plan2;         // per-mode plan words + hot-input caches (optional, host struct)
   const uint64_t* mkeys;      // per-mode stream (optional, alto_mode_stream): keys
   const void* mvals;          //   values
   int mtile;                  //   tile length T
   int mrr;                    //   round-robin slices (ALTO_MS_ROUND_ROBIN)
+  const int* mbase;           //   delta stream (ALTO_MS_DELTA): base row per lane group, else null
   int n_pairs;                // paired input modes (mode stream): count,
   int pair_a[2], pair_b[2];   //   modes,
   const void* pair_tab[2];    //   row-wise product tables (alto_krp_pair)

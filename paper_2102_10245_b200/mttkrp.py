@@ -44,9 +44,9 @@ CHUNK = 1 << 17
 # Elements per CTA tile of the streaming kernel.
 DEFAULT_TILE = 1024
 # float32 data with a float64 result: merge in float32 and upcast once.
-F32_ACCUMULATE = __import__("os").environ.get("ALTO_F32_ACCUMULATE", "1") == "1"
-# Streaming-kernel tuning switches (ALTO_STREAM_* in include/alto_b200.h).
-STREAM_FLAGS = int(__import__("os").environ.get("ALTO_STREAM_FLAGS", "0"))
+F32_ACCUMULATE = True
+# Streaming-kernel switches (ALTO_STREAM_* in include/alto_b200.h; 0 = default).
+STREAM_FLAGS = 0
 
 
 def _torch():
@@ -179,9 +179,6 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
     a.fixed_scale = None
     a.packed = None
     a.pos = None
-    a.plan = None
-    a.cache_k = 0
-    a.cache_modes = 0
     return a, cl
 
 
@@ -290,72 +287,21 @@ def _set_hot(a, tensor: AltoTensor, mode: int, rank: int, out_dtype, ms) -> None
                                                                    buf.data_ptr())
 
 
-# Shared-memory budget (bytes per CTA) for the hot-input row cache.
-CACHE_BUDGET = int(__import__("os").environ.get("ALTO_CACHE_BUDGET", 32 * 1024))
-# Default planned variant: "plan2" (plan words + hot-input cache) or "pos".
-PLAN_VARIANT = __import__("os").environ.get("ALTO_PLAN", "pos")
-
-
-def topk_rows(tensor: AltoTensor, mode: int, k: int):
-    """The k rows of `mode` with the most elements: (rows (k,) int32, slot map (I,) int32), cached."""
-    torch = _torch()
-    key = ("topk", mode, k)
-    hit = tensor._cache.get(key)
-    if hit is None:
-        lib = _lib.load()
-        dim = tensor.layout.dims[mode]
-        dev = tensor.keys.device
-        _perm, ptr = row_index(tensor, mode)
-        rows = torch.empty(k, dtype=torch.int32, device=dev)
-        smap = torch.empty(dim, dtype=torch.int32, device=dev)
-        wsb = lib.alto_topk_rows_workspace_bytes(dim)
-        ws = torch.empty(int(wsb), dtype=torch.uint8, device=dev)
-        _lib.check(lib.alto_topk_rows(ptr.data_ptr(), dim, k, rows.data_ptr(), smap.data_ptr(), ws.data_ptr(), wsb,
-                                      _lib.stream_ptr()), "alto_topk_rows")
-        hit = (rows, smap)
-        tensor._cache[key] = hit
-    return hit
-
-
-def stream_plan(tensor: AltoTensor, mode: int, rank: int, fbytes: int):
-    """Per-mode plan words (alto_stream_plan) + hot-input row caches, cached."""
-    torch = _torch()
-    order = tensor.layout.order
-    n_cache = min(order - 1, 3)
-    k = max(0, min(255, CACHE_BUDGET // max(1, n_cache * rank * fbytes)))
-    key = ("plan2", mode, k)
-    hit = tensor._cache.get(key)
-    if hit is not None:
-        return hit
-    lib = _lib.load()
-    in_modes = [n for n in range(order) if n != mode][:n_cache]
-    cache_rows, smaps = [], [None] * order
-    if k > 0:
-        for n in in_modes:
-            rows, smap = topk_rows(tensor, n, k)
-            cache_rows.append(rows)
-            smaps[n] = smap
-    hs = hot_slots(tensor, mode)
-    plan = torch.empty(max(tensor.nnz, 1), dtype=torch.int64, device=tensor.keys.device)
-    arr = (ctypes.c_void_p * order)(*[None if sm is None else sm.data_ptr() for sm in smaps])
-    _lib.check(lib.alto_stream_plan(c_layout(tensor.layout), packed_keys(tensor).data_ptr(), tensor.nnz, mode, arr,
-                                    None if hs is None else hs[0].data_ptr(), plan.data_ptr(), _lib.stream_ptr()),
-               "alto_stream_plan")
-    hit = {"plan": plan, "cache_rows": cache_rows, "k": k if cache_rows else 0, "modes": len(cache_rows)}
-    tensor._cache[key] = hit
-    return hit
-
-
 # Per-mode stream tile length (elements); 0 disables the mode-stream kernel.
-MS_TILE = int(__import__("os").environ.get("ALTO_MS_TILE", 1024))
+MS_TILE = 1024
 # Mode-stream order: 1 (default) = the whole stream sorted by the mode's
 # coordinate, ALTO order kept within a row (ALTO_MS_ROW_MAJOR); 0 = each tile
 # (a contiguous ALTO key range) sorted by it.
-MS_ORDER = int(__import__("os").environ.get("ALTO_MS_ORDER", 1))
+MS_ORDER = 1
 # Lane groups take round-robin positions of a tile (1, default: the 8 elements
 # of one warp instruction are consecutive, so their ALTO-ordered input rows
 # share lines more often) or contiguous slices (0).
-MS_RR = int(__import__("os").environ.get("ALTO_MS_RR", 1))
+MS_RR = 1
+# 128-bit layouts: store the mode stream with one key word per element (the
+# input coordinates + the row increment within the lane group, ALTO_MS_DELTA)
+# instead of two: 12 instead of 20 bytes per element on cfg3/cfg5.
+MS_DELTA = 1
+ALTO_MS_DELTA = 8
 
 
 def ms_tile(tensor: AltoTensor) -> int:
@@ -385,37 +331,55 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
         hs = hot_slots(tensor, mode)
         hot = hs is not None and lay.total_bits < 64 * lay.n_words
         ntiles = (m + T - 1) // T
-        skeys = torch.empty((max(ntiles * T, 1), lay.n_words), dtype=tensor.keys.dtype, device=dev)
-        svals = torch.empty(max(ntiles * T, 1), dtype=vals.dtype, device=dev)
         wsb = int(lib.alto_mode_stream_workspace_bytes(m))
         ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
-        rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals), m,
-                                  mode, T, MS_ORDER | (4 if MS_RR else 0), hs[0].data_ptr() if hot else None,
-                                  skeys.data_ptr(), svals.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr())
+        svals = torch.empty(max(ntiles * T, 1), dtype=vals.dtype, device=dev)
+        hit = None
+        if MS_DELTA and lay.n_words == 2 and MS_ORDER == 1:
+            # one key word per element: inputs + row increment (ALTO_MS_DELTA)
+            skeys = torch.empty((max(ntiles * T, 1), 1), dtype=tensor.keys.dtype, device=dev)
+            base = torch.empty(max(ntiles * 8, 1), dtype=torch.int32, device=dev)
+            ovf = torch.empty(1, dtype=torch.int32, device=dev)
+            rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals),
+                                      m, mode, T, MS_ORDER | (4 if MS_RR else 0) | ALTO_MS_DELTA,
+                                      hs[0].data_ptr() if hot else None, skeys.data_ptr(), svals.data_ptr(),
+                                      base.data_ptr(), ovf.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr())
+            if rc != _lib.ALTO_EUNSUPPORTED:
+                _lib.check(rc, "alto_mode_stream(delta)")
+                if int(ovf.item()) == 0:
+                    hit = (skeys, svals, T, MS_RR, base)
+            del skeys, base
+        if hit is None:
+            skeys = torch.empty((max(ntiles * T, 1), lay.n_words), dtype=tensor.keys.dtype, device=dev)
+            rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals),
+                                      m, mode, T, MS_ORDER | (4 if MS_RR else 0), hs[0].data_ptr() if hot else None,
+                                      skeys.data_ptr(), svals.data_ptr(), None, None, ws.data_ptr(), wsb,
+                                      _lib.stream_ptr())
+            if rc == _lib.ALTO_EUNSUPPORTED:
+                hit = False  # field layout does not fit the key width: planned kernel instead
+            else:
+                _lib.check(rc, "alto_mode_stream")
+                hit = (skeys, svals, T, MS_RR, None)
         del ws
-        if rc == _lib.ALTO_EUNSUPPORTED:
-            hit = False  # field layout does not fit the key width: planned kernel instead
-        else:
-            _lib.check(rc, "alto_mode_stream")
-            hit = (skeys, svals, T, MS_RR)
         tensor._cache[key] = hit
     return hit or None
 
 
 def _set_stream(a, ms) -> None:
-    sk, sv, st, rr = ms
+    sk, sv, st, rr, base = ms
     a.mkeys, a.mvals, a.mtile, a.mrr = sk.data_ptr(), sv.data_ptr(), st, 1 if rr else 0
+    a.mbase = None if base is None else base.data_ptr()
 
 
 # Ranks served by the mode-stream kernel (rank 32 stays on the planned kernel
 # unless listed: it measured no faster on cfg3).
-MS_RANKS = tuple(int(x) for x in __import__("os").environ.get("ALTO_MS_RANKS", "16").split(",") if x)
+MS_RANKS = (16,)
 
 
 # Paired input modes (orders 4-5, float32, rank 16): two input modes whose
 # row-wise product table (I_a * I_b rows) stays within MS_PAIR_BYTES are
 # gathered as one row, so one gather replaces two (0 disables pairing).
-MS_PAIR_BYTES = int(__import__("os").environ.get("ALTO_MS_PAIR_BYTES", 64 << 20))
+MS_PAIR_BYTES = 64 << 20
 
 
 def ms_pairs(dims, mode: int, rank: int, fbytes: int = 4, limit: int | None = None):
@@ -515,24 +479,17 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
                                                      _lib.stream_ptr()), "alto_cast_f32_f64")
         return out
     a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
-    ms = (mode_stream(tensor, mode) if planned is True and PLAN_VARIANT == "pos"
-          and _use_mode_stream(tensor, rank, fdev[0].element_size()) else None)
+    ms = (mode_stream(tensor, mode) if planned is True and _use_mode_stream(tensor, rank, fdev[0].element_size())
+          else None)
     if ms is not None:
         _set_stream(a, ms)
         tabs = []  # product tables: stream-ordered, released after the launch
         _set_pairs(a, tensor, fdev, mode, tabs)
     elif planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
             and max(tensor.layout.bits) <= 31:
+        # the single ALTO-order copy: packed keys + per-mode sub-tile order
         a.packed = packed_keys(tensor).data_ptr()
-        if planned == "pos" or (planned is True and PLAN_VARIANT == "pos"):
-            a.pos = subtile_order(tensor, mode).data_ptr()
-        else:
-            sp = stream_plan(tensor, mode, rank, fdev[0].element_size())
-            a.plan = sp["plan"].data_ptr()
-            for i, rws in enumerate(sp["cache_rows"]):
-                a.cache_rows[i] = rws.data_ptr()
-            a.cache_k = sp["k"]
-            a.cache_modes = sp["modes"]
+        a.pos = subtile_order(tensor, mode).data_ptr()
     if hot:
         _set_hot(a, tensor, mode, rank, out.dtype, ms)
     _lib.check(_lib.load().alto_mttkrp(ctypes.byref(a), _lib.stream_ptr()), "alto_mttkrp")
@@ -568,7 +525,7 @@ def pull_stream(tensor: AltoTensor, mode: int):
         ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
         rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals), m,
                                   mode, T, ALTO_MS_ROW_MAJOR, None, skeys.data_ptr(), svals.data_ptr(),
-                                  ws.data_ptr(), wsb, _lib.stream_ptr())
+                                  None, None, ws.data_ptr(), wsb, _lib.stream_ptr())
         del ws
         if rc == _lib.ALTO_EUNSUPPORTED:
             hit = False
@@ -745,7 +702,7 @@ def row_index(tensor: AltoTensor, mode: int):
 # Rows longer than this make the exact-order engine's sequential per-row sums
 # slow (a Zipf head row of 6.5M elements takes ~3 s); above it the
 # deterministic fixed-point streaming path is used instead.
-EXACT_MAX_RUN = int(__import__("os").environ.get("ALTO_EXACT_MAX_RUN", 65536))
+EXACT_MAX_RUN = 65536
 
 
 def max_row_length(tensor: AltoTensor, mode: int) -> int:
@@ -830,7 +787,7 @@ def mttkrp_det(tensor: AltoTensor, fdev: list, mode: int, out=None):
 # EXACT_MAX_RUN) run the exact-order engine, bitwise equal to the reference;
 # larger tensors run the K8/K9 pull engine (bitwise reproducible, ~1e-16
 # relative to the exact sums in float64).
-EXACT_MAX_NNZ = int(__import__("os").environ.get("ALTO_EXACT_MAX_NNZ", 4_000_000))
+EXACT_MAX_NNZ = 4_000_000
 
 
 def mttkrp_deterministic(tensor: AltoTensor, fdev: list, mode: int, part_offsets=None, out=None, out_dtype=None):

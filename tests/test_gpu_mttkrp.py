@@ -267,7 +267,7 @@ class TestStreamKernel:
         fdev = factors_to_device([rng.random((d, 16)).astype(np.float32) for d in dims])
         for mode in range(len(dims)):
             b = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=False).double().cpu().numpy()
-            for variant in (True, "pos", "plan2"):
+            for variant in (True, "pos"):
                 a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=variant).double().cpu().numpy()
                 assert rel_error(a, b) <= 1e-6, variant
 
@@ -299,18 +299,29 @@ class TestStreamKernel:
         for mode in range(len(dims)):
             ms = mk.mode_stream(alto, mode)
             assert ms is not None
-            sk, sv, tile, rr = ms
+            sk, sv, tile, rr, base = ms
             assert tile == T
-            sk = sk.cpu().numpy().view(np.uint64).reshape(-1, W)
+            delta = base is not None
+            assert delta == (W == 2 and order == 1)  # ALTO_MS_DELTA for 128-bit layouts, row-major streams
+            KW = 1 if delta else W
+            sk = sk.cpu().numpy().view(np.uint64).reshape(-1, KW)
             sv = sv.cpu().numpy()
             forder = [n for n in range(len(dims)) if n != mode] + [mode]
             cur, fields = 0, {}
             for n in forder:
                 b = lay.bits[n]
+                if delta and n == mode:
+                    b = min(31, 63 - cur)  # the row-increment field
                 if (cur % 64) + b > 64:
                     cur = (cur + 63) // 64 * 64
                 fields[n] = (cur // 64, cur % 64, b)
                 cur += b
+            if delta:  # rows = group base + running sum of increments
+                base = base.cpu().numpy()
+                inc = ((sk[:, 0] >> np.uint64(fields[mode][1])) & np.uint64((1 << fields[mode][2]) - 1)).astype(np.int64)
+                nt = (alto.nnz + T - 1) // T
+                g = inc[:nt * T].reshape(nt, T // 8, 8) if rr else inc[:nt * T].reshape(nt, T // 8, 8)
+                rows_all = (np.cumsum(g, axis=1) + base[:nt * 8].reshape(nt, 1, 8)).reshape(-1)
             hs = mk.hot_slots(alto, mode)
             hot_rows = set() if hs is None else set(hs[1][:hs[2]].cpu().numpy().tolist())
             ch = T // 8
@@ -322,7 +333,9 @@ class TestStreamKernel:
                 keys = sk[idx]
                 dec = np.stack([(keys[:, fields[n][0]] >> np.uint64(fields[n][1])) & np.uint64((1 << fields[n][2]) - 1)
                                 for n in range(len(dims))], 1).astype(np.int64)
-                flag = (keys[:, W - 1] >> np.uint64(63)).astype(bool)
+                if delta:
+                    dec[:, mode] = rows_all[idx]
+                flag = (keys[:, KW - 1] >> np.uint64(63)).astype(bool)
                 if order == 1:
                     ref = gperm[t0:t0 + cnt]
                 else:
