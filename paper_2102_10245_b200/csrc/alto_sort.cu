@@ -246,6 +246,175 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
   }
 }
 
+// --- one-sweep passes (decoupled look-back) ------------------------------------
+// Used when m < 2^30: one histogram kernel for every pass up front
+// (onesweep_hist + onesweep_scan: global digit bases), then per pass a single
+// kernel that reads each key/payload once and writes it once.  A CTA claims
+// the next tile in order (atomic counter), ranks it like radix_scatter,
+// publishes its per-digit counts (flag AGGREGATE), looks back over earlier
+// tiles until it finds an inclusive prefix (flag PREFIX), publishes its own,
+// and scatters the tile (staged digit-sorted in shared memory, coalesced
+// runs).  Tiles are claimed in order, so every tile a CTA waits on belongs to
+// a CTA that is already running.
+constexpr int kMaxPasses = 16;
+constexpr unsigned kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValMask = (1u << 30) - 1u;
+
+template <int W>
+__global__ void __launch_bounds__(kSortThreads) onesweep_hist(const uint64_t* __restrict__ keys, long long m,
+                                                              int passes, unsigned* __restrict__ ghist) {
+  __shared__ unsigned s_h[kMaxPasses * 256];
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m; i += stride) {
+    const Key<W> k = load_key<W>(keys, i);
+    for (int p = 0; p < passes; ++p) atomicAdd(&s_h[p * 256 + digit_of<W>(k, 8 * p)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+    if (s_h[i]) atomicAdd(ghist + i, s_h[i]);
+}
+
+__global__ void __launch_bounds__(256) onesweep_scan(unsigned* __restrict__ ghist) {
+  __shared__ unsigned s_tmp[32];
+  unsigned* h = ghist + static_cast<long long>(blockIdx.x) * 256;
+  const unsigned v = h[threadIdx.x];
+  unsigned total;
+  const unsigned ex = block_exclusive_scan(v, s_tmp, &total);
+  h[threadIdx.x] = ex;
+}
+
+__device__ __forceinline__ unsigned ld_status(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int W, int P>
+__global__ void __launch_bounds__(kSortThreads) onesweep_pass(const uint64_t* __restrict__ keys_in,
+                                                              const void* __restrict__ pay_in,
+                                                              uint64_t* __restrict__ keys_out,
+                                                              void* __restrict__ pay_out, long long m, int shift,
+                                                              const unsigned* __restrict__ gbase,
+                                                              unsigned* __restrict__ status,
+                                                              unsigned* __restrict__ tile_ctr) {
+  __shared__ unsigned s_warp[kSortWarps][256];
+  __shared__ unsigned s_base[256];
+  __shared__ unsigned s_dstart[256];
+  __shared__ unsigned s_scan[32];
+  __shared__ unsigned s_tile;
+  extern __shared__ __align__(16) unsigned char s_dyn[];  // digit-sorted tile: keys, then payload
+  uint64_t* s_keys = reinterpret_cast<uint64_t*>(s_dyn);
+  unsigned* s_pay32 = reinterpret_cast<unsigned*>(s_dyn + static_cast<size_t>(kSortTile) * W * 8);
+  uint64_t* s_pay64 = reinterpret_cast<uint64_t*>(s_dyn + static_cast<size_t>(kSortTile) * W * 8);
+  (void)s_pay32;
+  (void)s_pay64;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&s_warp[0][0])[i] = 0;
+  __syncthreads();
+  const long long tile = s_tile;
+  const long long base = tile * kSortTile + static_cast<long long>(warp) * kWarpSlice;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint64_t k0[kSortItems], k1[kSortItems];  // key words (k1 unused for W = 1)
+  uint64_t pv[kSortItems];
+  unsigned rd[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const long long i = base + j * 32 + lane;
+    const bool valid = i < m;
+    unsigned d = 0x100u + lane;  // invalid lanes: singleton groups
+    k0[j] = 0;
+    k1[j] = 0;
+    pv[j] = 0;
+    if (valid) {
+      const Key<W> kk = load_key<W>(keys_in, i);
+      k0[j] = kk.w[0];
+      if constexpr (W == 2) k1[j] = kk.w[1];
+      if constexpr (P == 4) pv[j] = static_cast<const unsigned*>(pay_in)[i];
+      if constexpr (P == 8) pv[j] = static_cast<const uint64_t*>(pay_in)[i];
+      d = digit_of<W>(kk, shift);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned r = __popc(peers & lt_mask);
+    unsigned prior = 0;
+    if (valid) prior = s_warp[warp][d];
+    __syncwarp();
+    if (valid && r == 0) s_warp[warp][d] = prior + __popc(peers);
+    __syncwarp();
+    rd[j] = ((prior + r) << 8) | (d & 0xffu);
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;
+    unsigned run = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      const unsigned c = s_warp[w][d];
+      s_warp[w][d] = run;
+      run += c;
+    }
+    unsigned total;
+    s_dstart[d] = block_exclusive_scan(run, s_scan, &total);
+    // decoupled look-back over the earlier tiles for digit d
+    unsigned* st = status + tile * 256 + d;
+    unsigned excl = 0;
+    if (tile == 0) {
+      st_status(st, kFlagPrefix | run);
+    } else {
+      st_status(st, kFlagAgg | run);
+      const unsigned* q = st - 256;
+      while (true) {
+        unsigned v;
+        do {
+          v = ld_status(q);
+        } while ((v & ~kValMask) == 0u);
+        excl += v & kValMask;
+        if ((v & ~kValMask) == kFlagPrefix) break;
+        q -= 256;
+      }
+      st_status(st, kFlagPrefix | (excl + run));
+    }
+    s_base[d] = gbase[d] + excl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const long long i = base + j * 32 + lane;
+    if (i < m) {
+      const unsigned d = rd[j] & 0xffu;
+      const unsigned lp = s_dstart[d] + s_warp[warp][d] + (rd[j] >> 8);
+      if constexpr (W == 1) {
+        s_keys[lp] = k0[j];
+      } else {
+        s_keys[2 * lp] = k0[j];
+        s_keys[2 * lp + 1] = k1[j];
+      }
+      if constexpr (P == 4) s_pay32[lp] = static_cast<unsigned>(pv[j]);
+      if constexpr (P == 8) s_pay64[lp] = pv[j];
+    }
+  }
+  __syncthreads();
+  const int cnt = static_cast<int>(min(static_cast<long long>(kSortTile), m - tile * kSortTile));
+  for (int lp = threadIdx.x; lp < cnt; lp += kSortThreads) {
+    Key<W> key;
+    if constexpr (W == 1) {
+      key.w[0] = s_keys[lp];
+    } else {
+      key.w[0] = s_keys[2 * lp];
+      key.w[1] = s_keys[2 * lp + 1];
+    }
+    const unsigned d = digit_of<W>(key, shift);
+    const long long dst = static_cast<long long>(s_base[d]) + (lp - s_dstart[d]);
+    store_key<W>(keys_out, dst, key);
+    if constexpr (P == 4) static_cast<unsigned*>(pay_out)[dst] = s_pay32[lp];
+    if constexpr (P == 8) static_cast<uint64_t*>(pay_out)[dst] = s_pay64[lp];
+  }
+}
+
 // --- K3 duplicates -----------------------------------------------------------
 
 template <int W>
@@ -268,8 +437,9 @@ __global__ void dup_fini(long long* p) {
 struct SortWs {
   uint64_t* keys_alt;
   void* pay_alt;
-  unsigned* counts;
+  unsigned* counts;   // per (digit, tile) counts; one-sweep: per (tile, digit) status words
   unsigned* partial;
+  unsigned* ghist;    // one-sweep: kMaxPasses x 256 digit bases + kMaxPasses tile counters
   size_t bytes;
 };
 
@@ -290,6 +460,8 @@ static SortWs carve(void* base, long long m, int W, int P) {
   off += align256(static_cast<size_t>(ncounts) * 4);
   w.partial = reinterpret_cast<unsigned*>(b ? b + off : nullptr);
   off += align256(static_cast<size_t>(nparts + 1) * 4);
+  w.ghist = reinterpret_cast<unsigned*>(b ? b + off : nullptr);
+  off += align256(static_cast<size_t>(kMaxPasses) * 257 * 4);
   w.bytes = off;
   return w;
 }
@@ -311,6 +483,25 @@ static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, con
   uint64_t* kout = ws.keys_alt;
   void* pin = pay;
   void* pout = ws.pay_alt;
+  if (m < (1ll << 30) && passes <= kMaxPasses) {
+    static bool os_attr = false;
+    if (!os_attr) {
+      ALTO_CUDA_TRY(cudaFuncSetAttribute(onesweep_pass<W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+      os_attr = true;
+    }
+    unsigned* ctr = ws.ghist + kMaxPasses * 256;
+    ALTO_CUDA_TRY(cudaMemsetAsync(ws.ghist, 0, static_cast<size_t>(kMaxPasses) * 257 * 4, s));
+    onesweep_hist<W><<<grid_for(m, kSortThreads, kSMs * 4), kSortThreads, 0, s>>>(kin, m, passes, ws.ghist);
+    onesweep_scan<<<passes, 256, 0, s>>>(ws.ghist);
+    for (int p = 0; p < passes; ++p) {
+      ALTO_CUDA_TRY(cudaMemsetAsync(ws.counts, 0, static_cast<size_t>(ncounts) * 4, s));
+      onesweep_pass<W, P><<<static_cast<unsigned>(ntiles), kSortThreads, smem, s>>>(
+          kin, pin, kout, pout, m, 8 * p, ws.ghist + p * 256, ws.counts, ctr + p);
+      std::swap(kin, kout);
+      std::swap(pin, pout);
+    }
+  } else {
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
     radix_hist<W><<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, m, shift, ws.counts, ntiles);
@@ -321,6 +512,7 @@ static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, con
                                                                                  ws.counts, ntiles);
     std::swap(kin, kout);
     std::swap(pin, pout);
+  }
   }
   ALTO_LAUNCH_CHECK("alto_sort_pairs");
   if (kin != keys) {
