@@ -110,11 +110,14 @@ int alto_partition(const alto_layout* lay, const void* d_tables,
 /* K6 — apply_boundary_flags (format.py:257-285): out_keys = keys with bit
  * flag_bit set on every element whose `mode` coordinate lies in one of its
  * partition's overlap ranges.  Overlaps in CSR form: partition l owns ranges
- * [ov_ptr[l], ov_ptr[l+1]) of (ov_lo[], ov_hi[]), ascending and disjoint. */
+ * [ov_ptr[l], ov_ptr[l+1]) of (ov_lo[], ov_hi[]), ascending and disjoint.
+ * d_offsets: the plan's partition offsets (count+1, device), any
+ * non-decreasing split of [0, m) as the reference accepts; NULL = the
+ * equal-size partition of `partition` (format.py:136-140). */
 int alto_apply_flags(const alto_layout* lay, const void* d_tables,
                      const uint64_t* keys, int64_t m, int64_t count,
                      int32_t mode, int32_t flag_bit, const int64_t* ov_ptr,
-                     const int64_t* ov_lo, const int64_t* ov_hi,
+                     const int64_t* ov_lo, const int64_t* ov_hi, const int64_t* d_offsets,
                      uint64_t* out_keys, void* stream);
 /* read_flags / clear_flags (format.py:288-299). */
 int alto_read_flags(const uint64_t* keys, int64_t m, int32_t n_words,

@@ -117,7 +117,7 @@ SIGNATURES = [
     ("alto_partition", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p,
                                  c_void_p]),
     ("alto_apply_flags", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int64, c_int32, c_int32,
-                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("alto_read_flags", c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     ("alto_clear_flags", c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     ("alto_mttkrp_ntiles", c_int64, [c_int64, c_int32]),

@@ -96,7 +96,7 @@ __global__ void flags_kernel(const __grid_constant__ DevLayout L, const uint64_t
                              const uint64_t* __restrict__ keys, long long m, long long base, long long extra,
                              int mode, int flag_bit, const long long* __restrict__ ov_ptr,
                              const long long* __restrict__ ov_lo, const long long* __restrict__ ov_hi,
-                             uint64_t* __restrict__ out) {
+                             const long long* __restrict__ offs, long long count, uint64_t* __restrict__ out) {
   extern __shared__ uint64_t s_dec[];
   copy_to_smem(s_dec, tab + static_cast<long long>(L.dec_off) * W, L.dec_bytes * 256 * W);
   __syncthreads();
@@ -105,7 +105,18 @@ __global__ void flags_kernel(const __grid_constant__ DevLayout L, const uint64_t
     Key<W> k = load_key<W>(keys, i);
     const Key<W> p = decode_packed<W>(s_dec, L.dec_bytes, k);
     const long long c = packed_field<W>(p, L.pack_off[mode], L.bits[mode]);
-    const long long l = partition_of(i, base, extra);
+    long long l;
+    if (offs) {
+      // arbitrary partition offsets: the last l with offs[l] <= i (skips empty partitions)
+      long long a0 = 0, b0 = count;
+      while (b0 - a0 > 1) {
+        const long long mid = (a0 + b0) >> 1;
+        if (offs[mid] <= i) a0 = mid; else b0 = mid;
+      }
+      l = a0;
+    } else {
+      l = partition_of(i, base, extra);
+    }
     long long a = ov_ptr[l], b = ov_ptr[l + 1];  // ranges [a, b)
     // last range with lo <= c
     while (a < b) {
@@ -224,11 +235,11 @@ int alto_partition(const alto_layout* lay, const void* d_tables, const uint64_t*
 
 int alto_apply_flags(const alto_layout* lay, const void* d_tables, const uint64_t* keys, int64_t m, int64_t count,
                      int32_t mode, int32_t flag_bit, const int64_t* ov_ptr, const int64_t* ov_lo,
-                     const int64_t* ov_hi, uint64_t* out_keys, void* stream) {
+                     const int64_t* ov_hi, const int64_t* d_offsets, uint64_t* out_keys, void* stream) {
   ALTO_REQUIRE(lay && lay->order >= 1 && lay->order <= ALTO_MAX_ORDER, "bad layout");
   ALTO_REQUIRE(mode >= 0 && mode < lay->order, "mode out of range");
   ALTO_REQUIRE(flag_bit >= lay->total_bits && flag_bit < 64 * lay->n_words, "flag bit must be an unused index bit");
-  ALTO_REQUIRE(count >= 1 && count <= (m > 1 ? m : 1), "partition count out of range");
+  ALTO_REQUIRE(count >= 1 && (d_offsets || count <= (m > 1 ? m : 1)), "partition count out of range");
   if (m <= 0) return ALTO_OK;
   const DevLayout d = make_dev_layout(lay);
   cudaStream_t s = as_stream(stream);
@@ -239,12 +250,15 @@ int alto_apply_flags(const alto_layout* lay, const void* d_tables, const uint64_
   auto* p = reinterpret_cast<const long long*>(ov_ptr);
   auto* lo = reinterpret_cast<const long long*>(ov_lo);
   auto* hi = reinterpret_cast<const long long*>(ov_hi);
+  auto* offs = reinterpret_cast<const long long*>(d_offsets);
   if (d.n_words == 1) {
     if (set_smem(flags_kernel<1>, smem)) return ALTO_ECUDA;
-    flags_kernel<1><<<grid, 256, smem, s>>>(d, tab, keys, m, base, extra, mode, flag_bit, p, lo, hi, out_keys);
+    flags_kernel<1><<<grid, 256, smem, s>>>(d, tab, keys, m, base, extra, mode, flag_bit, p, lo, hi, offs, count,
+                                            out_keys);
   } else {
     if (set_smem(flags_kernel<2>, smem)) return ALTO_ECUDA;
-    flags_kernel<2><<<grid, 256, smem, s>>>(d, tab, keys, m, base, extra, mode, flag_bit, p, lo, hi, out_keys);
+    flags_kernel<2><<<grid, 256, smem, s>>>(d, tab, keys, m, base, extra, mode, flag_bit, p, lo, hi, offs, count,
+                                            out_keys);
   }
   ALTO_LAUNCH_CHECK("alto_apply_flags");
   return ALTO_OK;

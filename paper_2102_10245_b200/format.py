@@ -320,9 +320,12 @@ def apply_boundary_flags(tensor: AltoTensor, plan: ConflictPlan) -> AltoTensor:
     count = len(offs) - 1
     if tensor.nnz == 0:
         return AltoTensor(tensor.layout, tensor.keys.clone(), tensor.vals)
-    expect = partition_offsets(tensor.nnz, count)
-    if not np.array_equal(offs, expect):
-        raise ValueError("plan offsets are not an equal-size partition of the tensor")
+    # any split of [0, nnz) the plan carries is accepted, as by the reference
+    # (format.py:274-284 loops over plan.offsets); equal-size splits use the
+    # closed form on device, others pass the offsets
+    d_offs = None
+    if not np.array_equal(offs, partition_offsets(tensor.nnz, count)):
+        d_offs = torch.from_numpy(offs.copy()).to(tensor.keys.device)
     ptr = np.zeros(count + 1, dtype=np.int64)
     ptr[1:] = np.cumsum([len(o) for o in plan.overlaps])
     flat = [r for o in plan.overlaps for r in o]
@@ -337,7 +340,8 @@ def apply_boundary_flags(tensor: AltoTensor, plan: ConflictPlan) -> AltoTensor:
     lay = tensor.layout
     _lib.check(lib.alto_apply_flags(c_layout(lay), device_tables(lay).data_ptr(), tensor.keys.data_ptr(), tensor.nnz,
                                     count, plan.mode, plan.flag_bit, d_ptr.data_ptr(), d_lo.data_ptr(),
-                                    d_hi.data_ptr(), out.data_ptr(), _lib.stream_ptr()), "alto_apply_flags")
+                                    d_hi.data_ptr(), None if d_offs is None else d_offs.data_ptr(), out.data_ptr(),
+                                    _lib.stream_ptr()), "alto_apply_flags")
     return AltoTensor(lay, out, tensor.vals)
 
 

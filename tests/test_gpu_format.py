@@ -147,6 +147,30 @@ class TestFlags:
             shared = {c for c, w in writers.items() if len(w) > 1}
             assert all(flags[i] for i in range(alto.nnz) if int(coords[i, mode]) in shared)
 
+    def test_arbitrary_offsets(self, at):
+        """Plans whose offsets are not the equal-size split (including empty
+        partitions) are flagged exactly as the reference does
+        (format.py:274-284 loops over plan.offsets)."""
+        alto = at.build_alto(at.random_tensor((30, 20, 16), 2000, seed=9))
+        lay = orc.build_layout(alto.layout.dims)
+        words = alto.indices
+        m = alto.nnz
+        offs = np.array([0, 5, 5, 400, 1111, m - 3, m], dtype=np.int64)
+        for mode in range(3):
+            base = at.plan_conflicts(alto, at.partition(alto, len(offs) - 1), mode,
+                                     force_strategy=at.Strategy.ATOMIC)
+            coords = orc.decode(lay, words, mode)
+            ovl = []
+            for l in range(len(offs) - 1):
+                mine = set(coords[offs[l]:offs[l + 1]].tolist())
+                other = set(coords[:offs[l]].tolist()) | set(coords[offs[l + 1]:].tolist())
+                rows = sorted(mine & other)
+                ovl.append(tuple((r, r) for r in rows))
+            plan = dataclasses.replace(base, offsets=offs, overlaps=tuple(ovl))
+            got = at.apply_boundary_flags(alto, plan).indices
+            want = orc.flag(lay, words, offs, mode, plan.overlaps, plan.flag_bit)
+            assert np.array_equal(got, want), mode
+
     def test_rejections(self, at, example_alto):
         parts = at.partition(example_alto, 2)
         buf = at.plan_conflicts(example_alto, parts, 0, force_strategy=at.Strategy.BUFFERED)
