@@ -378,12 +378,15 @@ typedef struct alto_pull_args {
   int64_t n_mseg;
   const int32_t* mseg;          /* (n_mseg,) segments with > 1 chunk         */
   double* part;                 /* (n_chunks, rank) float64 chunk partials   */
+  const int32_t* slice_rows;    /* (nslices, 2) first / last row per slice (alto_pull_slice_rows) */
+  const int32_t* mbase;         /* delta stream (ALTO_MS_DELTA): each slice's first row, else NULL */
 } alto_pull_args;
 int alto_mttkrp_pull(const alto_pull_args* a, void* stream);
 /* Plan helper: first and last output row of every slice of a mode stream,
- * first_last (nslices, 2) int32. */
+ * first_last (nslices, 2) int32; base = the delta stream's base rows (NULL
+ * for a plain stream). */
 int alto_pull_slice_rows(const alto_layout* lay, const uint64_t* mkeys, int64_t m, int32_t mode, int32_t tile,
-                         int32_t* first_last, void* stream);
+                         const int32_t* base, int32_t* first_last, void* stream);
 
 /* Exact-order engine (deterministic; bitwise equal to the reference for
  * float64 data): for mode `mode`, `row_perm` lists element indices sorted by

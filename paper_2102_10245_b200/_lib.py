@@ -99,6 +99,8 @@ class CPullArgs(Structure):
         ("n_mseg", c_int64),
         ("mseg", c_void_p),
         ("part", c_void_p),
+        ("slice_rows", c_void_p),
+        ("mbase", c_void_p),
     ]
 
 
@@ -146,7 +148,8 @@ SIGNATURES = [
                                  c_void_p, c_size_t, c_void_p]),
     ("alto_coord_max", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     ("alto_mttkrp_pull", c_int32, [POINTER(CPullArgs), c_void_p]),
-    ("alto_pull_slice_rows", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
+    ("alto_pull_slice_rows", c_int32, [POINTER(CLayout), c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p,
+                                       c_void_p]),
     ("alto_mttkrp_exact", c_int32, [POINTER(CMttkrpArgs), c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     ("alto_mttkrp_coo", c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, POINTER(c_void_p),
                                   c_void_p, c_int64, c_void_p]),

@@ -15,13 +15,14 @@ int alto_mttkrp_pull(const alto_pull_args* a, void* stream) {
   ALTO_REQUIRE(a->m >= 0 && a->m < (1ll << 32) - 1, "pull engine supports fewer than 2^32 elements");
   const DevLayout d = make_dev_layout(a->lay);
   for (int n = 0; n < d.order; ++n) ALTO_REQUIRE(d.bits[n] <= 31, "pull engine needs mode extents below 2^31");
-  const MsFields f = ms_fields(d, a->mode);
+  const bool delta = a->mbase != nullptr;
+  const MsFields f = delta ? ms_fields_delta(d, a->mode) : ms_fields(d, a->mode);
   if (!f.ok) {
     set_error("pull engine: the mode's field layout does not fit the key width");
     return ALTO_EUNSUPPORTED;
   }
   const long long dim = d.dims[a->mode];
-  ALTO_REQUIRE(a->m == 0 || (a->mkeys && a->mvals), "mode stream missing");
+  ALTO_REQUIRE(a->m == 0 || (a->mkeys && a->mvals && a->slice_rows), "mode stream or slice rows missing");
   ALTO_REQUIRE(a->atomic || a->m == 0 || a->slice_rec, "Buffered pull needs slice_rec");
   ALTO_REQUIRE(a->n_seg == 0 || a->seg_row, "shared rows missing");
   ALTO_REQUIRE(a->atomic || a->n_chunks == 0 || (a->rec && a->chunk_off && a->chunk_seg && a->seg_chunk_off &&
@@ -45,7 +46,9 @@ int alto_mttkrp_pull(const alto_pull_args* a, void* stream) {
   S.out = a->out;
   S.rec = a->rec;
   S.slice_rec = reinterpret_cast<const int2*>(a->slice_rec);
-  const int st = d.n_words == 1 ? pull_run_w1(a, S, d.order, s) : pull_run_w2(a, S, d.order, s);
+  S.slice_rows = reinterpret_cast<const int2*>(a->slice_rows);
+  const int st = delta ? pull_run_w1_delta(a, S, d.order, s)
+                       : (d.n_words == 1 ? pull_run_w1(a, S, d.order, s) : pull_run_w2(a, S, d.order, s));
   if (st == ALTO_EUNSUPPORTED)
     set_error("pull engine supports orders 3-5, ranks 16/32 (8/64 float32 Buffered) and dtypes "
               "f32/f32/f32, f32/f32/f64, f64/f64/f64, f32/f64/f64");
@@ -53,20 +56,21 @@ int alto_mttkrp_pull(const alto_pull_args* a, void* stream) {
 }
 
 int alto_pull_slice_rows(const alto_layout* lay, const uint64_t* mkeys, int64_t m, int32_t mode, int32_t tile,
-                         int32_t* first_last, void* stream) {
+                         const int32_t* base, int32_t* first_last, void* stream) {
   ALTO_REQUIRE(lay && mode >= 0 && mode < lay->order, "mode out of range");
   ALTO_REQUIRE(tile >= 128 && tile % 128 == 0, "tile must be a positive multiple of 128");
   if (m <= 0) return ALTO_OK;
   const DevLayout d = make_dev_layout(lay);
-  const MsFields f = ms_fields(d, mode);
+  const MsFields f = base ? ms_fields_delta(d, mode) : ms_fields(d, mode);
   ALTO_REQUIRE(f.ok, "the mode's field layout does not fit the key width");
   cudaStream_t s = as_stream(stream);
   const long long ns = (m + tile / 8 - 1) / (tile / 8);
   auto* fl = reinterpret_cast<int2*>(first_last);
-  if (d.n_words == 1)
-    pull_slice_rows_kernel<1><<<grid_for(ns, 256), 256, 0, s>>>(mkeys, m, tile, f, mode, fl);
+  const int* b = reinterpret_cast<const int*>(base);
+  if (d.n_words == 1 || base)
+    pull_slice_rows_kernel<1><<<grid_for(ns, 256), 256, 0, s>>>(mkeys, m, tile, f, mode, b, fl);
   else
-    pull_slice_rows_kernel<2><<<grid_for(ns, 256), 256, 0, s>>>(mkeys, m, tile, f, mode, fl);
+    pull_slice_rows_kernel<2><<<grid_for(ns, 256), 256, 0, s>>>(mkeys, m, tile, f, mode, b, fl);
   ALTO_LAUNCH_CHECK("alto_pull_slice_rows");
   return ALTO_OK;
 }

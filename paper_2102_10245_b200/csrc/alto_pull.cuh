@@ -55,6 +55,7 @@ struct PullStage {
   void* out;              // (dim, R) O
   void* rec;              // (n_rec, R) A: shared-row partials (Buffered)
   const int2* slice_rec;  // (nslices) record slot of the slice's first / last run, -1 if owned
+  const int2* slice_rows; // (nslices) first / last output row of every slice (alto_pull_slice_rows)
 };
 
 template <typename O, typename A>
@@ -91,7 +92,10 @@ __device__ __forceinline__ void red_row4(O* p, const A (&a)[4]) {
 }
 
 // V: stored value type, F: factor type (= accumulation type A), O: output.
-template <int W, typename V, typename F, typename O, int N, int R, int U, bool ATOMIC>
+// DELTA: one-word delta stream keys (ALTO_MS_DELTA): the output field holds the
+// row increment from the previous element of the slice; the slice's first row
+// comes from slice_rows.
+template <int W, typename V, typename F, typename O, int N, int R, int U, bool ATOMIC, bool DELTA = false>
 __global__ void __launch_bounds__(256, (sizeof(F) == 4 ? 3 : 2))
 pull_stage_kernel(const __grid_constant__ PullStage S) {
   using A = F;
@@ -123,11 +127,6 @@ pull_stage_kernel(const __grid_constant__ PullStage S) {
   const long long nblocks = (nslices + GPW - 1) / GPW;
   const long long w0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  // storage index of sorted position q
-  auto spos = [&](long long q) -> long long {
-    const long long g = q / CH;
-    return (g >> 3) * T + (q - g * CH) * 8 + (g & 7);
-  };
   for (long long sb = w0; sb < nblocks; sb += nw) {
     const long long g = sb * GPW + grp;
     const long long q0 = g * CH;
@@ -136,11 +135,12 @@ pull_stage_kernel(const __grid_constant__ PullStage S) {
     // neighbours' rows: the last element of slice g-1 and the first of g+1
     // (rows < 2^31; -1 = none)
     int prev_row = -1, next_row = -1;
+    unsigned carry = 0;  // DELTA: running row of the slice
     int2 slots = make_int2(-1, -1);
     if (len > 0) {
-      if (q0 > 0) prev_row = static_cast<int>(ms_field<W>(load_key_stream<W>(S.keys, spos(q0 - 1), pol), fout));
-      if (q0 + len < S.m)
-        next_row = static_cast<int>(ms_field<W>(load_key_stream<W>(S.keys, spos(q0 + len), pol), fout));
+      if (q0 > 0) prev_row = __ldg(S.slice_rows + g - 1).y;
+      if (q0 + len < S.m) next_row = __ldg(S.slice_rows + g + 1).x;
+      if constexpr (DELTA) carry = static_cast<unsigned>(__ldg(S.slice_rows + g).x);
       if constexpr (!ATOMIC) slots = __ldg(S.slice_rec + g);
     }
     int lw = prev_row;  // last output row written by or before this slice
@@ -202,7 +202,22 @@ pull_stage_kernel(const __grid_constant__ PullStage S) {
       unsigned mrow[NIN];
 #pragma unroll
       for (int k = 0; k < NIN; ++k) mrow[k] = ms_field<W>(kk, fin[k]);
-      const int mtg = (gl < U && j0 + gl < len) ? static_cast<int>(ms_field<W>(kk, fout)) : -1;
+      int mtg;
+      if constexpr (DELTA) {
+        // rows = carry + inclusive prefix of the U decoded increments
+        const bool ok = gl < U && j0 + gl < len;
+        unsigned dlt = ok ? ms_field<W>(kk, fout) : 0u;
+#pragma unroll
+        for (int o = 1; o < U; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, dlt, o, G);
+          if (gl >= o) dlt += y;
+        }
+        const unsigned row = carry + dlt;
+        carry = __shfl_sync(0xffffffffu, row, gbase + U - 1);
+        mtg = ok ? static_cast<int>(row) : -1;
+      } else {
+        mtg = (gl < U && j0 + gl < len) ? static_cast<int>(ms_field<W>(kk, fout)) : -1;
+      }
       V4<F> gv[U][NIN];
       int tg[U];
       A vu[U];
@@ -307,10 +322,12 @@ __global__ void zero_rows_kernel(const int* __restrict__ rows, long long n, int 
   }
 }
 
-// First and last output row of every slice (plan construction).
+// First and last output row of every slice (plan construction).  Delta
+// streams (base != null): first = base[g], last = first + the slice's
+// increments.
 template <int W>
 __global__ void pull_slice_rows_kernel(const uint64_t* __restrict__ keys, long long m, int tile, MsFields f, int mode,
-                                       int2* __restrict__ fl) {
+                                       const int* __restrict__ base, int2* __restrict__ fl) {
   const int CH = tile >> 3;
   const long long ns = (m + CH - 1) / CH;
   const FSel fo = fsel_of(f, mode);
@@ -319,9 +336,16 @@ __global__ void pull_slice_rows_kernel(const uint64_t* __restrict__ keys, long l
     const long long q0 = g * CH;
     const int len = static_cast<int>(min(static_cast<long long>(CH), m - q0));
     const long long sbase = (g >> 3) * tile + (g & 7);
-    const unsigned a = ms_field<W>(load_key<W>(keys, sbase), fo);
-    const unsigned z = ms_field<W>(load_key<W>(keys, sbase + static_cast<long long>(len - 1) * 8), fo);
-    fl[g] = make_int2(static_cast<int>(a), static_cast<int>(z));
+    if (base) {
+      unsigned r = static_cast<unsigned>(base[g]);
+      const unsigned a = r;
+      for (int j = 1; j < len; ++j) r += ms_field<W>(load_key<W>(keys, sbase + static_cast<long long>(j) * 8), fo);
+      fl[g] = make_int2(static_cast<int>(a), static_cast<int>(r));
+    } else {
+      const unsigned a = ms_field<W>(load_key<W>(keys, sbase), fo);
+      const unsigned z = ms_field<W>(load_key<W>(keys, sbase + static_cast<long long>(len - 1) * 8), fo);
+      fl[g] = make_int2(static_cast<int>(a), static_cast<int>(z));
+    }
   }
 }
 

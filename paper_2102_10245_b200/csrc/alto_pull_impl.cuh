@@ -14,11 +14,11 @@ constexpr int pull_u() {
   return std::min(R / 4, ub);
 }
 
-template <int W, typename V, typename F, typename O, int N, int R, bool AT>
+template <int W, typename V, typename F, typename O, int N, int R, bool AT, bool DELTA = false>
 int pull_launch(const alto_pull_args* a, const PullStage& S, cudaStream_t s) {
   using A = F;
   constexpr int U = pull_u<N, R, F>();
-  auto kern = pull_stage_kernel<W, V, F, O, N, R, U, AT>;
+  auto kern = pull_stage_kernel<W, V, F, O, N, R, U, AT, DELTA>;
   static int bps = 0;
   if (!bps) {
     int b = 1;
@@ -50,14 +50,14 @@ int pull_launch(const alto_pull_args* a, const PullStage& S, cudaStream_t s) {
   return ALTO_OK;
 }
 
-template <int W, typename V, typename F, typename O, bool AT>
+template <int W, typename V, typename F, typename O, bool AT, bool DELTA = false>
 int pull_by_shape(const alto_pull_args* a, const PullStage& S, int order, cudaStream_t s) {
   const int R = a->rank;
 #define ALTO_PULL_N(NN)                                                                  \
   if (order == NN) {                                                                     \
-    if (R == 16) return pull_launch<W, V, F, O, NN, 16, AT>(a, S, s);                    \
-    if (R == 32) return pull_launch<W, V, F, O, NN, 32, AT>(a, S, s);                    \
-    if constexpr (sizeof(F) == 4 && sizeof(O) == 4 && !AT) {                             \
+    if (R == 16) return pull_launch<W, V, F, O, NN, 16, AT, DELTA>(a, S, s);             \
+    if (R == 32) return pull_launch<W, V, F, O, NN, 32, AT, DELTA>(a, S, s);             \
+    if constexpr (sizeof(F) == 4 && sizeof(O) == 4 && !AT && !DELTA) {                   \
       if (R == 8) return pull_launch<W, V, F, O, NN, 8, AT>(a, S, s);                    \
       if (R == 64) return pull_launch<W, V, F, O, NN, 64, AT>(a, S, s);                  \
     }                                                                                    \
@@ -74,6 +74,22 @@ int pull_by_atomic(const alto_pull_args* a, const PullStage& S, int order, cudaS
   return a->atomic ? pull_by_shape<W, V, F, O, true>(a, S, order, s) : pull_by_shape<W, V, F, O, false>(a, S, order, s);
 }
 
+// One-word delta streams (float32 values: the 128-bit-key configs).
+inline int pull_run_delta(const alto_pull_args* a, const PullStage& S, int order, cudaStream_t s) {
+  const int vd = a->value_dtype, fd = a->factor_dtype, od = a->out_dtype;
+  if (vd != ALTO_F32) return ALTO_EUNSUPPORTED;
+  if (fd == ALTO_F32 && od == ALTO_F32)
+    return a->atomic ? pull_by_shape<1, float, float, float, true, true>(a, S, order, s)
+                     : pull_by_shape<1, float, float, float, false, true>(a, S, order, s);
+  if (fd == ALTO_F32 && od == ALTO_F64)
+    return a->atomic ? pull_by_shape<1, float, float, double, true, true>(a, S, order, s)
+                     : pull_by_shape<1, float, float, double, false, true>(a, S, order, s);
+  if (fd == ALTO_F64 && od == ALTO_F64)
+    return a->atomic ? pull_by_shape<1, float, double, double, true, true>(a, S, order, s)
+                     : pull_by_shape<1, float, double, double, false, true>(a, S, order, s);
+  return ALTO_EUNSUPPORTED;
+}
+
 template <int W>
 int pull_run(const alto_pull_args* a, const PullStage& S, int order, cudaStream_t s) {
   const int vd = a->value_dtype, fd = a->factor_dtype, od = a->out_dtype;
@@ -86,5 +102,6 @@ int pull_run(const alto_pull_args* a, const PullStage& S, int order, cudaStream_
 
 int pull_run_w1(const alto_pull_args* a, const PullStage& S, int order, cudaStream_t s);
 int pull_run_w2(const alto_pull_args* a, const PullStage& S, int order, cudaStream_t s);
+int pull_run_w1_delta(const alto_pull_args* a, const PullStage& S, int order, cudaStream_t s);
 
 }  // namespace alto

@@ -506,8 +506,10 @@ def pull_stream(tensor: AltoTensor, mode: int):
     """The mode's row-major stream with contiguous slices (alto_mode_stream,
     ALTO_MS_ROW_MAJOR): the ALTO elements stably sorted by the output
     coordinate, ALTO order kept inside a row, cached per (mode, tile) like the
-    reference's per-mode plans (_make_backend, cpd.py:149-181).
-    -> (keys, values, tile) or None when the field layout does not fit."""
+    reference's per-mode plans (_make_backend, cpd.py:149-181).  128-bit
+    layouts use one-word delta keys (ALTO_MS_DELTA) when the increments fit.
+    -> (keys, values, tile, base rows or None) or None when the field layout
+    does not fit."""
     torch = _torch()
     T = ms_tile(tensor)
     key = ("pstream", mode, T)
@@ -519,19 +521,32 @@ def pull_stream(tensor: AltoTensor, mode: int):
         dev = tensor.keys.device
         vals = tensor.vals
         ntiles = (m + T - 1) // T
-        skeys = torch.empty((max(ntiles * T, 1), lay.n_words), dtype=tensor.keys.dtype, device=dev)
         svals = torch.empty(max(ntiles * T, 1), dtype=vals.dtype, device=dev)
         wsb = int(lib.alto_mode_stream_workspace_bytes(m))
         ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
-        rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals), m,
-                                  mode, T, ALTO_MS_ROW_MAJOR, None, skeys.data_ptr(), svals.data_ptr(),
-                                  None, None, ws.data_ptr(), wsb, _lib.stream_ptr())
+        if MS_DELTA and lay.n_words == 2 and vals.dtype == torch.float32:
+            skeys = torch.empty((max(ntiles * T, 1), 1), dtype=tensor.keys.dtype, device=dev)
+            base = torch.empty(max(ntiles * 8, 1), dtype=torch.int32, device=dev)
+            ovf = torch.empty(1, dtype=torch.int32, device=dev)
+            rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals),
+                                      m, mode, T, ALTO_MS_ROW_MAJOR | ALTO_MS_DELTA, None, skeys.data_ptr(),
+                                      svals.data_ptr(), base.data_ptr(), ovf.data_ptr(), ws.data_ptr(), wsb,
+                                      _lib.stream_ptr())
+            if rc != _lib.ALTO_EUNSUPPORTED:
+                _lib.check(rc, "alto_mode_stream(delta)")
+                if int(ovf.item()) == 0:
+                    hit = (skeys, svals, T, base)
+        if hit is None:
+            skeys = torch.empty((max(ntiles * T, 1), lay.n_words), dtype=tensor.keys.dtype, device=dev)
+            rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals),
+                                      m, mode, T, ALTO_MS_ROW_MAJOR, None, skeys.data_ptr(), svals.data_ptr(),
+                                      None, None, ws.data_ptr(), wsb, _lib.stream_ptr())
+            if rc == _lib.ALTO_EUNSUPPORTED:
+                hit = False
+            else:
+                _lib.check(rc, "alto_mode_stream")
+                hit = (skeys, svals, T, None)
         del ws
-        if rc == _lib.ALTO_EUNSUPPORTED:
-            hit = False
-        else:
-            _lib.check(rc, "alto_mode_stream")
-            hit = (skeys, svals, T)
         tensor._cache[key] = hit
     return hit or None
 
@@ -560,7 +575,8 @@ def pull_plan(tensor: AltoTensor, mode: int):
     ns = (m + ch - 1) // ch
     fl = torch.empty((max(ns, 1), 2), dtype=torch.int32, device=dev)
     _lib.check(_lib.load().alto_pull_slice_rows(c_layout(tensor.layout), ps[0].data_ptr(), m, mode, T,
-                                                fl.data_ptr(), _lib.stream_ptr()), "alto_pull_slice_rows")
+                                                None if ps[3] is None else ps[3].data_ptr(), fl.data_ptr(),
+                                                _lib.stream_ptr()), "alto_pull_slice_rows")
     first, last = fl[:ns, 0].long(), fl[:ns, 1].long()
     sf = torch.zeros(ns, dtype=torch.bool, device=dev)
     sl = torch.zeros(ns, dtype=torch.bool, device=dev)
@@ -600,7 +616,7 @@ def pull_plan(tensor: AltoTensor, mode: int):
         chunk_seg = torch.zeros(1, dtype=torch.int32, device=dev)
         mseg = torch.zeros(0, dtype=torch.int32, device=dev)
         n_chunks = 0
-    hit = {"slice_rec": slice_rec, "n_rec": n_rec, "seg_row": seg_row, "n_seg": int(seg_row.numel()) if n_rec else 0,
+    hit = {"slice_rows": fl, "slice_rec": slice_rec, "n_rec": n_rec, "seg_row": seg_row, "n_seg": int(seg_row.numel()) if n_rec else 0,
            "chunk_off": chunk_off, "chunk_seg": chunk_seg, "seg_chunk_off": seg_chunk_off, "n_chunks": n_chunks,
            "mseg": mseg, "n_mseg": int(mseg.numel())}
     tensor._cache[key] = hit
@@ -658,6 +674,8 @@ def mttkrp_pull(tensor: AltoTensor, fdev: list, mode: int, out=None, out_dtype=N
         a.factors[n] = f.data_ptr()
     a.out = out.data_ptr()
     a.slice_rec = plan["slice_rec"].data_ptr()
+    a.slice_rows = plan["slice_rows"].data_ptr()
+    a.mbase = None if ps[3] is None else ps[3].data_ptr()
     rec = part = None
     if not atomic and plan["n_rec"]:
         rec = torch.empty((plan["n_rec"], rank), dtype=fdev[0].dtype, device=out.device)
