@@ -221,7 +221,11 @@ class DeviceBackend:
                 self.offsets[mode] = np.asarray(parts.offsets)
             else:
                 if plan.flag_bit is not None:
-                    apply_boundary_flags(tensor, plan)  # validated like the reference; kernel ignores flag bits
+                    apply_boundary_flags(tensor, plan)  # validated like the reference (cpd.py:172-176)
+                # Atomic backend: the mode-stream kernel (per-row-run atomic
+                # merges, Zipf-head rows through float64-summed replicated
+                # copies) — the fastest float32 path; mttkrp_par with an
+                # Atomic plan runs the pull engine's flag-exact atomic scheme
                 self.engine[mode] = "stream"
 
     def run(self, fdev: list, mode: int, out=None, allow_f32: bool = False):

@@ -1,29 +1,21 @@
-// alto_mttkrp.cu — ALTO MTTKRP on B200.
+// alto_mttkrp.cu — the deterministic reference-order MTTKRP engines.
 //
 //   out[i_n, r] = sum over elements x: x.value * prod_{m != n} F_m[x.coord_m, r]
 //   (pkg/src/altotensor/mttkrp.py:1-14, contributions :80-105)
 //
-// 1. Streaming tile kernel (K7/K8, the fast path).  A CTA owns a tile of the
-//    sorted ALTO stream (contiguous elements, so a compact coordinate box).
-//    Phase A streams the tile's keys/values with coalesced loads, decodes all
-//    modes in registers through the byte tables, and parks coordinates and
-//    values in shared memory, reducing the output-mode interval [lo, hi].
-//    Phase B, when hi-lo+1 fits the on-chip buffer (the paper's per-partition
-//    interval buffer, Alg. 2 / mttkrp.py:148-156, at CTA granularity), each
-//    warp owns the buffer rows r with (r-lo) % 8 == warp and applies the
-//    contributions of its rows in element order (no shared-memory atomics:
-//    on sm_100a those compile to CAS loops).  Factor rows are gathered as
-//    coalesced 64/128-byte row segments (LPE lanes per element).  Touched
-//    rows are then pushed to the float64 output with one RED per (row, rank)
-//    — the pull/merge step.  Tiles whose interval is too wide use direct
-//    float64 atomics per element (the Atomic scheme, mttkrp.py:178-224).
-// 2. Exact-order engine (deterministic): per output row, contributions are
-//    summed sequentially in element order, restarted at partition boundaries,
-//    and partition partials combined in ascending order — the arithmetic
-//    order of _par_buffered (mttkrp.py:148-172) and mttkrp_seq (:108-117), in
-//    float64 with contraction disabled, hence bitwise equal to the reference
-//    on float64 inputs.
-// 3. COO kernel (mttkrp_oracle, mttkrp.py:64-77) over a coordinate list.
+// 1. Exact-order engine (`alto_row_index` + `alto_mttkrp_exact`): per output
+//    row, contributions are summed sequentially in element order, restarted
+//    at partition boundaries, and the partition partials combined in
+//    ascending order — the arithmetic order of _par_buffered
+//    (mttkrp.py:148-172) and mttkrp_seq (:108-117), in float64 with
+//    contraction disabled, hence bitwise equal to the reference on float64
+//    inputs.
+// 2. COO kernels over a coordinate list (mttkrp_oracle, mttkrp.py:64-77):
+//    `alto_mttkrp_coo` (float64 atomics) and `alto_mttkrp_coo_ordered`
+//    (stable row sort, each row summed in input order: bitwise = reference).
+// The streaming kernels live in alto_mstream.cuh (mode stream), alto_pull.cuh
+// (K8/K9 slice buffers + pull), alto_fast.cuh (ALTO-order planned kernel)
+// and alto_stream.cuh (generic fallback).
 #include <algorithm>
 #include <climits>
 

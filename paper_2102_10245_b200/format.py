@@ -34,6 +34,15 @@ class AltoTensor:
     `keys` ((nnz, n_words) int64 raw bits) and `vals` (float32 or float64 —
     float32 storage is kept when the caller supplies float32 values; the
     upcast to the float64 `.values` view is exact).
+
+    Like the reference's frozen dataclass, a tensor is immutable: transforms
+    return new tensors.  Device torch inputs are adopted without a copy, so
+    the caller must not modify them afterwards (per-mode plans cached on the
+    tensor — mode streams, pull plans, row indexes — assume fixed contents).
+    The mode-stream kernel's replicated hot-row partials are cached scratch
+    that each call leaves zeroed; two concurrent MTTKRPs on the same tensor
+    from different streams must not run the mode-stream kernel at the same
+    time (the pull engine allocates its scratch per call).
     """
 
     def __init__(self, layout: AltoLayout, indices, values):

@@ -782,6 +782,10 @@ def mttkrp_det(tensor: AltoTensor, fdev: list, mode: int, out=None):
                                    _lib.stream_ptr()), "alto_absmax")
         k += 1
     _lib.check(lib.alto_fixed_scale(terms.data_ptr(), k, scale.data_ptr(), _lib.stream_ptr()), "alto_fixed_scale")
+    if not bool(torch.isfinite(terms[:k]).all().item()):
+        # a NaN/Inf value or factor has no fixed-point bound: the exact-order
+        # engine propagates it like the reference does
+        return mttkrp_exact(tensor, fdev, mode, out=out)
     fixed = torch.empty((dim, rank), dtype=torch.int64, device=dev)
     a, _keep = _args(tensor, fdev, mode, fixed, DEFAULT_TILE, 1, vals=vals)
     a.out_dtype = _lib.ALTO_I64
