@@ -349,7 +349,7 @@ class DeviceCpAls:
         replayed: every kernel and workspace is static by then (plans,
         hot-row copies and launch configurations are cached), and a replay
         removes the host launch gaps between the ~30 small launches of a
-        sweep.  Set CPD_GRAPHS = False (ALTO_CPD_GRAPHS=0) to run eagerly."""
+        sweep.  Set CPD_GRAPHS = False to run eagerly."""
         torch = _torch()
         order = self.tensor.layout.order
         if not CPD_GRAPHS or self._graph is False:
