@@ -37,7 +37,10 @@ constexpr int kScanChunk = kScanThreads * kScanItems;  // 4096 counters
 
 template <int W>
 __device__ __forceinline__ unsigned digit_of(const Key<W>& k, int shift) {
-  return static_cast<unsigned>(k.w[shift >> 6] >> (shift & 63)) & 0xffu;
+  // select the word without dynamic indexing (which would place the key in local memory)
+  uint64_t w = k.w[0];
+  if constexpr (W == 2) w = shift >= 64 ? k.w[1] : k.w[0];
+  return static_cast<unsigned>(w >> (shift & 63)) & 0xffu;
 }
 
 template <int W>
