@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
 // runs).  Tiles are claimed in order, so every tile a CTA waits on belongs to
 // a CTA that is already running.
 constexpr int kMaxPasses = 16;
+constexpr int kOnesweepThreads = 512;  // one-sweep CTA: 4096-key tiles
 constexpr unsigned kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValMask = (1u << 30) - 1u;
 
 template <int W>
@@ -296,31 +297,33 @@ __device__ __forceinline__ void st_status(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int W, int P>
-__global__ void __launch_bounds__(kSortThreads) onesweep_pass(const uint64_t* __restrict__ keys_in,
+// OT threads per CTA, tile = OT * kSortItems keys; threads < 256 own one digit.
+template <int W, int P, int OT>
+__global__ void __launch_bounds__(OT, 1024 / OT) onesweep_pass(const uint64_t* __restrict__ keys_in,
                                                               const void* __restrict__ pay_in,
                                                               uint64_t* __restrict__ keys_out,
                                                               void* __restrict__ pay_out, long long m, int shift,
                                                               const unsigned* __restrict__ gbase,
                                                               unsigned* __restrict__ status,
                                                               unsigned* __restrict__ tile_ctr) {
-  __shared__ unsigned s_warp[kSortWarps][256];
+  constexpr int NW = OT / 32, TILE = OT * kSortItems, SLICE = TILE / NW;
+  __shared__ unsigned s_warp[NW][256];
   __shared__ unsigned s_base[256];
   __shared__ unsigned s_dstart[256];
   __shared__ unsigned s_scan[32];
   __shared__ unsigned s_tile;
   extern __shared__ __align__(16) unsigned char s_dyn[];  // digit-sorted tile: keys, then payload
   uint64_t* s_keys = reinterpret_cast<uint64_t*>(s_dyn);
-  unsigned* s_pay32 = reinterpret_cast<unsigned*>(s_dyn + static_cast<size_t>(kSortTile) * W * 8);
-  uint64_t* s_pay64 = reinterpret_cast<uint64_t*>(s_dyn + static_cast<size_t>(kSortTile) * W * 8);
+  unsigned* s_pay32 = reinterpret_cast<unsigned*>(s_dyn + static_cast<size_t>(TILE) * W * 8);
+  uint64_t* s_pay64 = reinterpret_cast<uint64_t*>(s_dyn + static_cast<size_t>(TILE) * W * 8);
   (void)s_pay32;
   (void)s_pay64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&s_warp[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < NW * 256; i += blockDim.x) (&s_warp[0][0])[i] = 0;
   __syncthreads();
   const long long tile = s_tile;
-  const long long base = tile * kSortTile + static_cast<long long>(warp) * kWarpSlice;
+  const long long base = tile * TILE + static_cast<long long>(warp) * SLICE;
   const unsigned lt_mask = (1u << lane) - 1u;
   uint64_t k0[kSortItems], k1[kSortItems];  // key words (k1 unused for W = 1)
   uint64_t pv[kSortItems];
@@ -351,17 +354,24 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const uint64_t* __
     rd[j] = ((prior + r) << 8) | (d & 0xffu);
   }
   __syncthreads();
-  {
-    const int d = threadIdx.x;
-    unsigned run = 0;
+  // per-digit exclusive scan over warps (stable order of warps) and the
+  // tile-local exclusive scan over digits; thread d < 256 owns digit d
+  const int d = threadIdx.x;
+  unsigned run = 0;
+  if (d < 256) {
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const unsigned c = s_warp[w][d];
       s_warp[w][d] = run;
       run += c;
     }
+  }
+  {
     unsigned total;
-    s_dstart[d] = block_exclusive_scan(run, s_scan, &total);
+    const unsigned ds = block_exclusive_scan(run, s_scan, &total);
+    if (d < 256) s_dstart[d] = ds;
+  }
+  if (d < 256) {
     // decoupled look-back over the earlier tiles for digit d
     unsigned* st = status + tile * 256 + d;
     unsigned excl = 0;
@@ -401,8 +411,8 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const uint64_t* __
     }
   }
   __syncthreads();
-  const int cnt = static_cast<int>(min(static_cast<long long>(kSortTile), m - tile * kSortTile));
-  for (int lp = threadIdx.x; lp < cnt; lp += kSortThreads) {
+  const int cnt = static_cast<int>(min(static_cast<long long>(TILE), m - tile * TILE));
+  for (int lp = threadIdx.x; lp < cnt; lp += OT) {
     Key<W> key;
     if constexpr (W == 1) {
       key.w[0] = s_keys[lp];
@@ -487,10 +497,13 @@ static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, con
   void* pin = pay;
   void* pout = ws.pay_alt;
   if (m < (1ll << 30) && passes <= kMaxPasses) {
+    constexpr int OT = kOnesweepThreads;
+    const long long otiles = (m + OT * kSortItems - 1) / (OT * kSortItems);
+    const size_t osmem = static_cast<size_t>(OT) * kSortItems * (W * 8 + P);
     static bool os_attr = false;
     if (!os_attr) {
-      ALTO_CUDA_TRY(cudaFuncSetAttribute(onesweep_pass<W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
+      ALTO_CUDA_TRY(cudaFuncSetAttribute(onesweep_pass<W, P, OT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(osmem)));
       os_attr = true;
     }
     unsigned* ctr = ws.ghist + kMaxPasses * 256;
@@ -498,8 +511,8 @@ static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, con
     onesweep_hist<W><<<grid_for(m, kSortThreads, kSMs * 4), kSortThreads, 0, s>>>(kin, m, passes, ws.ghist);
     onesweep_scan<<<passes, 256, 0, s>>>(ws.ghist);
     for (int p = 0; p < passes; ++p) {
-      ALTO_CUDA_TRY(cudaMemsetAsync(ws.counts, 0, static_cast<size_t>(ncounts) * 4, s));
-      onesweep_pass<W, P><<<static_cast<unsigned>(ntiles), kSortThreads, smem, s>>>(
+      ALTO_CUDA_TRY(cudaMemsetAsync(ws.counts, 0, static_cast<size_t>(otiles) * 256 * 4, s));
+      onesweep_pass<W, P, OT><<<static_cast<unsigned>(otiles), OT, osmem, s>>>(
           kin, pin, kout, pout, m, 8 * p, ws.ghist + p * 256, ws.counts, ctr + p);
       std::swap(kin, kout);
       std::swap(pin, pout);
