@@ -500,6 +500,12 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
 # Records per level-1 pull chunk (kPullChunk in csrc/alto_pull.cuh).
 PULL_CHUNK = 64
 ALTO_MS_ROW_MAJOR = 1
+# Pull-stream tile for large tensors (slices of PULL_TILE / 8 stream
+# positions; >= 8 slices per resident lane group), else the mode-stream tile.
+# Measured on cfg5 (ms per mode): 1024 -> 6.82 / 6.70 / 7.25, 2048 -> 6.57 /
+# 6.47 / 6.96, 4096 -> 6.43 / 6.32 / 6.83, 8192 -> 6.45 / 6.39 / 6.87
+# (fewer boundary records, longer runs); shorter slices are slower.
+PULL_TILE = 4096
 
 
 def pull_stream(tensor: AltoTensor, mode: int):
@@ -511,7 +517,7 @@ def pull_stream(tensor: AltoTensor, mode: int):
     -> (keys, values, tile, base rows or None) or None when the field layout
     does not fit."""
     torch = _torch()
-    T = ms_tile(tensor)
+    T = PULL_TILE if tensor.nnz >= 148 * 24 * 8 * PULL_TILE else ms_tile(tensor)
     key = ("pstream", mode, T)
     hit = tensor._cache.get(key)
     if hit is None:
