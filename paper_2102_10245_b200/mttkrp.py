@@ -371,9 +371,10 @@ def _set_stream(a, ms) -> None:
     a.mbase = None if base is None else base.data_ptr()
 
 
-# Ranks served by the mode-stream kernel (rank 32 stays on the planned kernel
-# unless listed: it measured no faster on cfg3).
-MS_RANKS = (16,)
+# Ranks served by the mode-stream kernel (others: the planned ALTO-order
+# kernel).  Rank 32 joined in round 2: with one-word delta keys cfg3 modes
+# 0-1 run 2.74 / 2.64 ms vs 2.90 / 2.78 on the planned kernel.
+MS_RANKS = (16, 32)
 
 
 # Paired input modes (orders 4-5, float32, rank 16): two input modes whose
