@@ -456,7 +456,7 @@ def run_b200(args):
                          "achieved_gbs": ba / (mode_ms[n] * 1e-3) / 1e9, "nnz_per_s": M / (mode_ms[n] * 1e-3)})
     tot_b = sum(p["bytes_alg"] for p in per_mode)
     achieved = tot_b / (sum(mode_ms) * 1e-3) / 1e9
-    ms_used = all(alto._cache.get(("mstream", n, alto.vals.dtype, mk.ms_tile(alto), mk.MS_ORDER, mk.MS_RR))
+    ms_used = all(any(k[0] == "mstream" and k[1] == n and v for k, v in alto._cache.items() if isinstance(k, tuple))
                   for n in range(N))
     kernel_name = "alto::mstream_kernel (alto_mstream.cuh)" if ms_used else "alto::planned_kernel (alto_fast.cuh)"
     launches_per_step = 0

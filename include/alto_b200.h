@@ -189,7 +189,7 @@ typedef struct alto_mttkrp_args {
    * the per-slot first copy (n_hot+1), and hot_buf hot_base[n_hot] * rank
    * elements of out_dtype (zero on entry, left zero). */
   const int32_t* hot_base;
-  int32_t mrr;                   /* mode stream built with ALTO_MS_ROUND_ROBIN */
+  int32_t mrr;                   /* mode stream built with ALTO_MS_ROUND_ROBIN (1) or ALTO_MS_BLOCKED (2) */
   /* Paired input modes (mode stream only; float32 values and factors, rank
    * 16, orders 4-5): input modes pair_a[i], pair_b[i] (i < n_pairs, disjoint,
    * not `mode`) are gathered together as one row of pair_tab[i], the
@@ -266,6 +266,19 @@ size_t alto_mode_stream_workspace_bytes(int64_t m);
                            ALTO_EUNSUPPORTED if fewer than 8 increment bits are left, and
                            *d_overflow (device int32, zeroed by the call) is set when an increment
                            does not fit (the caller then builds a plain stream) */
+#define ALTO_MS_BLOCKED 16 /* flags (row-major only): a warp step covers groups*u consecutive sorted
+                              elements; lane group s takes elements s, s+groups, ... of the step and
+                              its u elements are stored contiguously (sorted element k*groups+s of a
+                              step at s*u+k); delta increments refer to the element `groups`
+                              positions earlier and base_rows holds ntiles * groups rows.  u and
+                              groups come from alto_mstream_block, passed as ALTO_MS_BLOCK(u, groups) */
+#define ALTO_MS_BLOCK(u, groups) (ALTO_MS_BLOCKED | ((u) << 8) | ((groups) << 12))
+/* Step shape of the blocked mode-stream kernel for a tensor order, rank,
+ * value dtype and number of paired input modes: *u elements per lane group
+ * and *groups lane groups per warp (ALTO_EUNSUPPORTED when no kernel covers
+ * the shape). */
+int alto_mstream_block(int32_t order, int32_t rank, int32_t value_dtype, int32_t n_pairs, int32_t* u,
+                       int32_t* groups);
 int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,
                      int64_t m, int32_t mode, int32_t tile, int32_t flags, const int32_t* hot_slot,
                      uint64_t* skeys, void* svals, int32_t* base_rows, int32_t* d_overflow,

@@ -139,6 +139,7 @@ SIGNATURES = [
     ("alto_mode_stream", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32,
                                    c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                    c_void_p]),
+    ("alto_mstream_block", c_int32, [c_int32, c_int32, c_int32, c_int32, POINTER(c_int32), POINTER(c_int32)]),
     ("alto_topk_rows_workspace_bytes", c_size_t, [c_int64]),
     ("alto_hot_rows", c_int32, [c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_size_t, c_void_p]),

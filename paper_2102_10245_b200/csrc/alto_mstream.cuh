@@ -343,6 +343,208 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
   }
 }
 
+// Stream loads of NB bytes (16-byte pieces) that all lanes of a group issue
+// on the same address (one broadcast request for the warp's GPW groups).
+template <int NB>
+__device__ __forceinline__ void load_stream_bytes(unsigned (&dst)[NB / 4], const void* p, unsigned long long pol) {
+  static_assert(NB == 4 || NB == 8 || NB % 16 == 0, "4, 8 or a multiple of 16 bytes");
+  if constexpr (NB == 4) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(dst[0]) : "l"(p), "l"(pol));
+  } else if constexpr (NB == 8) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+        : "=r"(dst[0]), "=r"(dst[1])
+        : "l"(p), "l"(pol));
+  } else {
+#pragma unroll
+    for (int i = 0; i < NB / 16; ++i)
+      asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+          : "=r"(dst[4 * i]), "=r"(dst[4 * i + 1]), "=r"(dst[4 * i + 2]), "=r"(dst[4 * i + 3])
+          : "l"(static_cast<const char*>(p) + 16 * i), "l"(pol));
+  }
+}
+
+// Field selectors of the blocked kernel's gathered inputs, resolved on the
+// host in gather order so the kernel reads them from the parameter bank with
+// compile-time indices (a selector indexed by `mode` at run time costs
+// SEL/LEA/LDC per field per element once registers are short).
+struct MsSel {
+  unsigned sh, mask, hi;  // hi: field lives in the key's last word
+};
+struct MsBlk {
+  MsSel in[ALTO_MAX_ORDER];   // gathered input k: row field (pairs: the a field)
+  MsSel inb[ALTO_MAX_ORDER];  //   pairs: the b field (mask 0 when unpaired)
+  unsigned vdb[ALTO_MAX_ORDER];  // pairs: I_b (1 when unpaired)
+  const void* tab[ALTO_MAX_ORDER];  // factor or product table of input k
+  MsSel out;                  // output row (or row increment) field
+};
+
+template <int W>
+__device__ __forceinline__ unsigned ms_sel(const Key<W>& k, const MsSel& f) {
+  if constexpr (W == 1) {
+    return static_cast<unsigned>(k.w[0] >> f.sh) & f.mask;
+  } else {
+    const uint64_t w = f.hi ? k.w[W - 1] : k.w[0];
+    return static_cast<unsigned>(w >> f.sh) & f.mask;
+  }
+}
+
+// Blocked mode-stream kernel (ALTO_MS_BLOCKED).  A warp step covers B = GPW*U
+// consecutive sorted elements; lane group s takes elements s, s+GPW, ... of
+// the step (round robin: the GPW elements of one gather instruction are
+// consecutive, so their ALTO-ordered input rows share lines) and the stream
+// stores those U elements contiguously (element u*GPW+s of a step at s*U+u).
+// Every lane of a group reads the group's U keys and U values itself with
+// 16-byte accesses on group-uniform addresses (broadcast) and decodes them
+// redundantly, so no shuffle is left in the element loop (the cooperative
+// decode above spends 19 shuffles per 32 elements, ~20 % of the load/store
+// pipe's wavefronts on cfg5).  Delta streams: the increment is taken from the
+// group's previous element (GPW positions earlier); base[tile * GPW + s]
+// holds the row of the group's first element.
+// The next step's keys and values are prefetched into registers.  Measured
+// (profiles/r02e_ab_blocked.jsonl): faster than the cooperative kernel at
+// rank 32 (cfg3 2.64-2.77 -> 2.32-2.38 ms per mode) and for orders 4-5 (cfg4
+// 0.265 -> 0.239 ms), slower at order 3 / rank 16 (cfg2 0.46 -> 0.50 ms:
+// a broadcast 16-byte load still costs 4 data-pipe wavefronts, 512 bytes of
+// register writeback, so the load/store pipe total does not drop there while
+// the redundant decode adds instructions) — the host picks per shape.  A
+// variant staging the stream through shared memory with cp.async (no
+// prefetch registers) was slower everywhere (cfg2 0.53, cfg3 3.0-3.4 ms).
+template <int W, typename V, typename O, int N, int R, int MINB, int U, int NV, bool DELTA>
+__global__ void __launch_bounds__(kTileThreads, MINB)
+mstream_blk_kernel(const __grid_constant__ MStream S, const __grid_constant__ MsBlk Q,
+                   const __grid_constant__ StreamParams P) {
+  using F = V;
+  using A = V;
+  constexpr int G = R / 4;
+  constexpr int GPW = 32 / G;
+  constexpr int B = GPW * U;
+  constexpr int NIN = NV;
+  constexpr bool PAIR = NV < N - 1;
+  constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
+  constexpr unsigned HOTF = 0x80000000u;
+  constexpr int KB = U * W * 8;                           // key bytes of a group per step
+  constexpr int VB = U * static_cast<int>(sizeof(V));     // value bytes of a group per step
+  constexpr int KSTEP = B * W * 8;                        // key bytes of a warp step
+  constexpr int VSTEP = B * static_cast<int>(sizeof(V));  // value bytes of a warp step
+  const int T = S.tile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const unsigned qmask = (G >= 4) ? (0xFu << (lane & ~3)) : 0xffffffffu;
+  // byte offset of input k's gathered row for key kk
+  auto voff = [&](const Key<W>& kk, int k) -> unsigned {
+    if constexpr (PAIR)
+      return (ms_sel<W>(kk, Q.in[k]) * Q.vdb[k] + ms_sel<W>(kk, Q.inb[k])) * ROWB;
+    else
+      return ms_sel<W>(kk, Q.in[k]) * ROWB;
+  };
+  O* __restrict__ out = static_cast<O*>(P.out);
+  const double fixed_scale = P.fixed_scale ? *P.fixed_scale : 1.0;
+  const int* __restrict__ hot_code = P.n_hot > 0 ? P.hot_slot : nullptr;
+  O* __restrict__ hot_buf = static_cast<O*>(P.hot_buf);
+  const unsigned hotmask = hot_code ? HOTF : 0u;
+  const unsigned long long pol = stream_policy(!(P.flags & ALTO_STREAM_MS_L2_NORMAL));
+
+  const long long ntiles = (P.m + T - 1) / T;
+  const long long gw0 = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp;
+  const long long nwarps = static_cast<long long>(gridDim.x) * (kTileThreads / 32);
+  if (gw0 >= ntiles) return;
+  unsigned next_base = 0;
+  if constexpr (DELTA) next_base = static_cast<unsigned>(__ldg(S.base + gw0 * GPW + grp));
+  for (long long t = gw0; t < ntiles; t += nwarps) {
+    const long long tb = t * T;
+    const int cnt = static_cast<int>(min(static_cast<long long>(T), P.m - tb));
+    A acc[4] = {A(0), A(0), A(0), A(0)};
+    unsigned cur = 0xffffffffu;
+    auto flush = [&]() {
+      O* base;
+      if (cur & HOTF) {
+        const int hc = __ldg(hot_code + (cur & ~HOTF));
+        base = hot_buf + (static_cast<long long>(hc >> 5) + (static_cast<unsigned>(t) & ((1u << (hc & 31)) - 1u))) * R;
+      } else {
+        base = out + static_cast<long long>(cur) * R;
+      }
+      merge_row<O, A, G, R>(base, acc, gl, qmask, lane, fixed_scale);
+    };
+    auto consume = [&](unsigned tgt, V v, const V4<F> (&gg)[NIN]) {
+      A tv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tv[q] = static_cast<A>(v) * static_cast<A>(gg[0].v[q]);
+#pragma unroll
+      for (int k = 1; k < NIN - 1; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tv[q] *= static_cast<A>(gg[k].v[q]);
+      if (tgt == cur) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = fma(tv[q], static_cast<A>(gg[NIN - 1].v[q]), acc[q]);
+      } else {
+        if (cur != 0xffffffffu) flush();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = tv[q] * static_cast<A>(gg[NIN - 1].v[q]);
+        cur = tgt;
+      }
+    };
+    unsigned carry = 0;
+    if constexpr (DELTA) {
+      carry = next_base;
+      if (t + nwarps < ntiles) next_base = static_cast<unsigned>(__ldg(S.base + (t + nwarps) * GPW + grp));
+    }
+    const char* kp = reinterpret_cast<const char*>(S.keys) + (tb + grp * U) * (W * 8);
+    const char* vp = static_cast<const char*>(S.vals) + (tb + grp * U) * static_cast<long long>(sizeof(V));
+    unsigned nkw[KB / 4], nvw[VB / 4];  // next step's keys / values
+    load_stream_bytes<KB>(nkw, kp, pol);
+    load_stream_bytes<VB>(nvw, vp, pol);
+    const int nsteps = (cnt + B - 1) / B;
+#pragma unroll 1
+    for (int jb = 0; jb < nsteps; ++jb) {
+      unsigned kw[KB / 4], vw[VB / 4];  // keys / values of the step being consumed
+#pragma unroll
+      for (int i = 0; i < KB / 4; ++i) kw[i] = nkw[i];
+#pragma unroll
+      for (int i = 0; i < VB / 4; ++i) vw[i] = nvw[i];
+      if (jb + 1 < nsteps) {
+        load_stream_bytes<KB>(nkw, kp + static_cast<long long>(jb + 1) * KSTEP, pol);
+        load_stream_bytes<VB>(nvw, vp + static_cast<long long>(jb + 1) * VSTEP, pol);
+      }
+      const int e0 = jb * B + grp;  // sorted position of the group's first element of the step
+      unsigned tg[U];
+      V4<F> g[U][NIN];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        Key<W> kk;
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          kk.w[w] = (static_cast<uint64_t>(kw[(u * W + w) * 2 + 1]) << 32) | kw[(u * W + w) * 2];
+        const bool ok = e0 + u * GPW < cnt;
+        unsigned row;
+        if constexpr (DELTA) {
+          carry += ok ? ms_sel<W>(kk, Q.out) : 0u;
+          row = carry;
+        } else {
+          row = ms_sel<W>(kk, Q.out);
+        }
+        tg[u] = ok ? (row | (kw[(u * W + W - 1) * 2 + 1] & hotmask)) : 0xffffffffu;
+        if (ok) {
+#pragma unroll
+          for (int k = 0; k < NIN; ++k)
+            g[u][k] = gather_off<F>(static_cast<const char*>(Q.tab[k]) + 4 * sizeof(F) * gl, voff(kk, k));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (tg[u] != 0xffffffffu) {
+          V v;
+          if constexpr (sizeof(V) == 4)
+            v = __uint_as_float(vw[u]);
+          else
+            v = __hiloint2double(static_cast<int>(vw[2 * u + 1]), static_cast<int>(vw[2 * u]));
+          consume(tg[u], v, g[u]);
+        }
+    }
+    if (cur != 0xffffffffu) flush();
+  }
+}
+
 // Elements in flight per group: ~UREG registers of gathered factor data per
 // lane, at most one decoding lane per element (U <= G).
 template <int N, int R, typename V, int UREG>
@@ -354,6 +556,43 @@ constexpr int ms_u() {
 template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = ms_u<N, R, V, 32>(), int NV = N - 1,
           bool DELTA = false>
 int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, cudaStream_t s) {
+  if (S.rr == 2) {
+    // blocked stream (ALTO_MS_BLOCKED): broadcast vector loads, redundant decode, no shuffles
+    constexpr int GPW = 32 / (R / 4);
+    if (S.tile % (GPW * U)) return ALTO_EUNSUPPORTED;
+    MsBlk Q{};
+    constexpr bool PAIR = NV < N - 1;
+    for (int k = 0; k < NV; ++k) {
+      int na, nb = -1;
+      if (PAIR) {
+        na = S.vin[k].na;
+        nb = S.vin[k].nb;
+        Q.tab[k] = S.vin[k].tab;
+        Q.vdb[k] = nb >= 0 ? S.vin[k].db : 1u;
+      } else {
+        na = k < P.mode ? k : k + 1;
+        Q.tab[k] = P.factors[na];
+        Q.vdb[k] = 1u;
+      }
+      Q.in[k] = MsSel{static_cast<unsigned>(S.f.sh[na]), S.f.mask[na], S.f.word[na] != 0 ? 1u : 0u};
+      Q.inb[k] = nb >= 0 ? MsSel{static_cast<unsigned>(S.f.sh[nb]), S.f.mask[nb], S.f.word[nb] != 0 ? 1u : 0u}
+                         : MsSel{0u, 0u, 0u};
+    }
+    Q.out = MsSel{static_cast<unsigned>(S.f.sh[P.mode]), S.f.mask[P.mode], S.f.word[P.mode] != 0 ? 1u : 0u};
+    auto kern = mstream_blk_kernel<W, V, O, N, R, MINB, U, NV, DELTA>;
+    static int blk_bps = 0;
+    if (!blk_bps) {
+      int b = 1;
+      ALTO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kTileThreads, 0));
+      blk_bps = std::max(b, 1);
+    }
+    const long long ntiles = (P.m + S.tile - 1) / S.tile;
+    const long long need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);
+    const long long grid = std::min<long long>(need, static_cast<long long>(device_sms()) * blk_bps);
+    kern<<<static_cast<unsigned>(grid), kTileThreads, 0, s>>>(S, Q, P);
+    ALTO_LAUNCH_CHECK("alto_mttkrp(blocked mode stream)");
+    return ALTO_OK;
+  }
   auto kern = mstream_kernel<W, V, O, N, R, MINB, U, NV, DELTA>;
   static int cached_bps = 0;
   if (!cached_bps) {

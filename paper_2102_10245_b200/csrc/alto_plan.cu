@@ -119,7 +119,7 @@ __global__ void mstream_scatter_kernel(const __grid_constant__ DevLayout L, cons
                                        int round_robin, const int* __restrict__ hot_slot,
                                        uint64_t* __restrict__ skeys, V* __restrict__ svals,
                                        const uint64_t* __restrict__ srows, int* __restrict__ base_rows,
-                                       int* __restrict__ overflow) {
+                                       int* __restrict__ overflow, int blk_u, int blk_gpw) {
   const int ch = tile / kMsSlices;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < m; q += stride) {
@@ -129,16 +129,33 @@ __global__ void mstream_scatter_kernel(const __grid_constant__ DevLayout L, cons
     // slices: lane group s takes sorted positions [s*ch, (s+1)*ch) of the tile,
     // stored interleaved; round robin: group s takes positions s, s+8, ...
     // (consecutive elements in one instruction), stored in sorted order
-    const long long dst = round_robin ? q : t * tile + static_cast<long long>(p % ch) * kMsSlices + p / ch;
+    long long dst = round_robin ? q : t * tile + static_cast<long long>(p % ch) * kMsSlices + p / ch;
+    if (round_robin == 2) {
+      // blocked: a warp step is blk_gpw * blk_u consecutive sorted elements;
+      // group s takes elements s, s + gpw, ... of the step (round robin) and
+      // its blk_u elements are stored contiguously (one vector load)
+      const int bsz = blk_gpw * blk_u;
+      const int pb = p % bsz;
+      dst = q - pb + (pb % blk_gpw) * blk_u + pb / blk_gpw;
+    }
     const Key<W> k = load_key<W>(packed, src);
     const unsigned row = packed_field32<W>(k, L.pack_off[mode], L.bits[mode]);
     const bool hot = hot_slot && hot_slot[row] >= 0;
     if (base_rows) {
       // delta stream: inputs + increment from the group's previous element
       // (srows = the sorted row of every position, so its neighbour is known)
-      const int gs = round_robin ? (p % kMsSlices) : (p / ch);
-      const int gj = round_robin ? (p / kMsSlices) : (p % ch);
-      const long long prev = round_robin ? q - kMsSlices : q - 1;
+      const bool rr1 = round_robin == 1;
+      int gs = rr1 ? (p % kMsSlices) : (p / ch);
+      int gj = rr1 ? (p / kMsSlices) : (p % ch);
+      long long prev = rr1 ? q - kMsSlices : q - 1;
+      int ngroups = kMsSlices;
+      if (round_robin == 2) {
+        // blocked: group s takes sorted positions s, s + gpw, ... of the tile
+        gs = p % blk_gpw;
+        gj = p / blk_gpw;
+        prev = q - blk_gpw;
+        ngroups = blk_gpw;
+      }
       uint64_t w = 0;
       for (int n = 0; n < L.order; ++n) {
         if (n == mode) continue;
@@ -146,7 +163,7 @@ __global__ void mstream_scatter_kernel(const __grid_constant__ DevLayout L, cons
       }
       unsigned dlt = 0;
       if (gj == 0) {
-        base_rows[t * kMsSlices + gs] = static_cast<int>(row);
+        base_rows[t * ngroups + gs] = static_cast<int>(row);
       } else {
         dlt = row - static_cast<unsigned>(srows[prev]);
         if (dlt > F.mask[mode]) atomicExch(overflow, 1);
@@ -231,6 +248,12 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
   const bool delta = (flags & ALTO_MS_DELTA) != 0;
   ALTO_REQUIRE(!delta || ((flags & ALTO_MS_ROW_MAJOR) && base_rows && d_overflow),
                "delta stream needs row-major order, base_rows and d_overflow");
+  const bool blocked = (flags & ALTO_MS_BLOCKED) != 0;
+  const int blk_u = (flags >> 8) & 15, blk_gpw = (flags >> 12) & 15;
+  ALTO_REQUIRE(!blocked || ((flags & ALTO_MS_ROW_MAJOR) && blk_u >= 1 && blk_u <= 8 && blk_gpw >= 1 && blk_gpw <= 8 &&
+                            tile % (blk_u * blk_gpw) == 0),
+               "blocked stream needs row-major order and ALTO_MS_BLOCK(u, groups) dividing the tile");
+  const int gmode = blocked ? 2 : ((flags & ALTO_MS_ROUND_ROBIN) ? 1 : 0);
   const MsFields F = delta ? ms_fields_delta(d, mode) : ms_fields(d, mode);
   if (!F.ok) {
     set_error("mode stream: the mode's field layout does not fit the key width");
@@ -269,9 +292,9 @@ int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void*
   const int* hs = reinterpret_cast<const int*>(hot_slot);
 #define ALTO_MS_SCATTER(WW, VT)                                                                              \
   mstream_scatter_kernel<WW, VT><<<grid, 256, 0, s>>>(d, F, packed, static_cast<const VT*>(values), idx, m, mode, \
-                                                      tile, (flags & ALTO_MS_ROUND_ROBIN) ? 1 : 0, hs, skeys,    \
-                                                      static_cast<VT*>(svals), delta ? ckey : nullptr,           \
-                                                      delta ? base_rows : nullptr, d_overflow)
+                                                      tile, gmode, hs,                                            \
+                                                      skeys, static_cast<VT*>(svals), delta ? ckey : nullptr,    \
+                                                      delta ? base_rows : nullptr, d_overflow, blk_u, blk_gpw)
   if (d.n_words == 1) {
     if (vb == 4) ALTO_MS_SCATTER(1, float); else ALTO_MS_SCATTER(1, double);
   } else {

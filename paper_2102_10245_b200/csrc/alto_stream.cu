@@ -239,6 +239,22 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   return ALTO_OK;
 }
 
+int alto_mstream_block(int32_t order, int32_t rank, int32_t value_dtype, int32_t n_pairs, int32_t* u,
+                       int32_t* groups) {
+  ALTO_REQUIRE(u && groups, "null output");
+  ALTO_REQUIRE(value_dtype == ALTO_F32 || value_dtype == ALTO_F64, "unsupported value dtype");
+  if (order < 3 || order > 5 || (rank != 16 && rank != 32) || n_pairs < 0 || n_pairs > 2 ||
+      order - 1 - n_pairs < 2)
+    return ALTO_EUNSUPPORTED;
+  // same rule as ms_u<NV + 1, R, V, 32>() (alto_mstream.cuh): ~32 registers of
+  // gathered factor data per lane, at most R/4 elements per group
+  const int nv = order - 1 - n_pairs;
+  const int vw = value_dtype == ALTO_F32 ? 1 : 2;
+  *u = std::min(rank / 4, std::max(1, 32 / (nv * 4 * vw)));
+  *groups = 128 / rank;
+  return ALTO_OK;
+}
+
 int alto_hot_copies(const int64_t* row_ptr, const int32_t* hot_rows, int32_t n_hot, int64_t m, int32_t tile,
                     int32_t flags, int32_t bound, int32_t max_lg, int32_t* hot_code, int32_t* hot_base,
                     void* stream) {

@@ -293,15 +293,22 @@ MS_TILE = 1024
 # coordinate, ALTO order kept within a row (ALTO_MS_ROW_MAJOR); 0 = each tile
 # (a contiguous ALTO key range) sorted by it.
 MS_ORDER = 1
-# Lane groups take round-robin positions of a tile (1, default: the 8 elements
-# of one warp instruction are consecutive, so their ALTO-ordered input rows
-# share lines more often) or contiguous slices (0).
-MS_RR = 1
+# Lane groups of a warp.  1 = round-robin positions s, s+8, ... of a tile
+# (cooperative decode + shuffles); 0 = contiguous slices; 2 (default) = the
+# blocked kernel (ALTO_MS_BLOCKED: same round-robin assignment, each group's
+# elements of a warp step stored contiguously, every lane loads its group's
+# keys/values itself with broadcast vector loads, no shuffles) for the shapes
+# it wins on — rank 32 and orders 4-5: cfg3 2.64-2.77 -> 2.32-2.38 ms, cfg4
+# 0.265 -> 0.239 ms per mode — and round robin for order 3 / rank 16, where it
+# loses (cfg2 0.46 -> 0.50, cfg5 6.1 -> 6.6 ms; profiles/r02e_ab_blocked.jsonl);
+# 3 = blocked wherever it exists.  Tile-ordered streams (MS_ORDER 0) use 1.
+MS_RR = 2
 # 128-bit layouts: store the mode stream with one key word per element (the
 # input coordinates + the row increment within the lane group, ALTO_MS_DELTA)
 # instead of two: 12 instead of 20 bytes per element on cfg3/cfg5.
 MS_DELTA = 1
 ALTO_MS_DELTA = 8
+ALTO_MS_BLOCKED = 16
 
 
 def ms_tile(tensor: AltoTensor) -> int:
@@ -314,14 +321,53 @@ def ms_tile(tensor: AltoTensor) -> int:
     return t
 
 
-def mode_stream(tensor: AltoTensor, mode: int, vals=None):
+def ms_block(order: int, rank: int, vals_dtype_code: int, n_pairs: int):
+    """(u, groups) of the blocked mode-stream kernel's warp step
+    (alto_mstream_block), or None when no blocked kernel covers the shape."""
+    u, g = ctypes.c_int32(0), ctypes.c_int32(0)
+    rc = _lib.load().alto_mstream_block(order, rank, vals_dtype_code, n_pairs, ctypes.byref(u), ctypes.byref(g))
+    if rc == _lib.ALTO_EUNSUPPORTED:
+        return None
+    _lib.check(rc, "alto_mstream_block")
+    return int(u.value), int(g.value)
+
+
+def _ms_group_mode(tensor: AltoTensor, vals, rank: int, n_pairs: int):
+    """-> (rr, blk): the lane-group assignment the stream is built for.
+    MS_RR = 2 picks the blocked kernel for the shapes it is the measured
+    winner on (rank 32, orders 4-5; float32) and round robin elsewhere;
+    MS_RR = 3 forces it wherever a blocked kernel exists (tests)."""
+    torch = _torch()
+    rr = MS_RR if MS_ORDER == 1 else min(MS_RR, 1)
+    if rr == 2 and not (vals.dtype == torch.float32 and (rank == 32 or tensor.layout.order >= 4)):
+        rr = 1
+    rr = min(rr, 2)
+    blk = ms_block(tensor.layout.order, rank, _dt_code(vals), n_pairs) if rr == 2 else None
+    if rr == 2 and blk is None:
+        rr = 1
+    return rr, blk
+
+
+def mode_stream_key(tensor: AltoTensor, mode: int, vals=None, rank: int = 16, n_pairs: int = 0):
+    """Cache key of mode_stream (a blocked stream's storage order and delta
+    encoding depend on the kernel's step shape)."""
+    vals = tensor.vals if vals is None else vals
+    rr, blk = _ms_group_mode(tensor, vals, rank, n_pairs)
+    return ("mstream", mode, vals.dtype, ms_tile(tensor), MS_ORDER, rr, blk)
+
+
+def mode_stream(tensor: AltoTensor, mode: int, vals=None, rank: int = 16, n_pairs: int = 0):
     """Per-mode stream of the MTTKRP (alto_mode_stream), cached per (mode,
-    value dtype): the ALTO stream in tiles of MS_TILE elements, each stably
-    sorted by its `mode` coordinate, with hot-row flags.  -> (keys, values, tile)."""
+    value dtype, lane-group assignment): the ALTO elements stably sorted by
+    their `mode` coordinate (ALTO order kept within a row; tile by tile when
+    MS_ORDER is 0), with hot-row flags.  `rank` / `n_pairs` select the blocked
+    kernel's step shape.  -> (keys, values, tile, rr, base rows or None)."""
     torch = _torch()
     vals = tensor.vals if vals is None else vals
     T = ms_tile(tensor)
-    key = ("mstream", mode, vals.dtype, T, MS_ORDER, MS_RR)
+    rr, blk = _ms_group_mode(tensor, vals, rank, n_pairs)
+    gflags = {0: 0, 1: 4}.get(rr, 0) if rr != 2 else (ALTO_MS_BLOCKED | (blk[0] << 8) | (blk[1] << 12))
+    key = mode_stream_key(tensor, mode, vals, rank, n_pairs)
     hit = tensor._cache.get(key)
     if hit is None:
         lib = _lib.load()
@@ -341,25 +387,25 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
             base = torch.empty(max(ntiles * 8, 1), dtype=torch.int32, device=dev)
             ovf = torch.empty(1, dtype=torch.int32, device=dev)
             rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals),
-                                      m, mode, T, MS_ORDER | (4 if MS_RR else 0) | ALTO_MS_DELTA,
+                                      m, mode, T, MS_ORDER | gflags | ALTO_MS_DELTA,
                                       hs[0].data_ptr() if hot else None, skeys.data_ptr(), svals.data_ptr(),
                                       base.data_ptr(), ovf.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr())
             if rc != _lib.ALTO_EUNSUPPORTED:
                 _lib.check(rc, "alto_mode_stream(delta)")
                 if int(ovf.item()) == 0:
-                    hit = (skeys, svals, T, MS_RR, base)
+                    hit = (skeys, svals, T, rr, base)
             del skeys, base
         if hit is None:
             skeys = torch.empty((max(ntiles * T, 1), lay.n_words), dtype=tensor.keys.dtype, device=dev)
             rc = lib.alto_mode_stream(c_layout(lay), packed_keys(tensor).data_ptr(), vals.data_ptr(), _dt_code(vals),
-                                      m, mode, T, MS_ORDER | (4 if MS_RR else 0), hs[0].data_ptr() if hot else None,
+                                      m, mode, T, MS_ORDER | gflags, hs[0].data_ptr() if hot else None,
                                       skeys.data_ptr(), svals.data_ptr(), None, None, ws.data_ptr(), wsb,
                                       _lib.stream_ptr())
             if rc == _lib.ALTO_EUNSUPPORTED:
                 hit = False  # field layout does not fit the key width: planned kernel instead
             else:
                 _lib.check(rc, "alto_mode_stream")
-                hit = (skeys, svals, T, MS_RR, None)
+                hit = (skeys, svals, T, rr, None)
         del ws
         tensor._cache[key] = hit
     return hit or None
@@ -367,7 +413,7 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None):
 
 def _set_stream(a, ms) -> None:
     sk, sv, st, rr, base = ms
-    a.mkeys, a.mvals, a.mtile, a.mrr = sk.data_ptr(), sv.data_ptr(), st, 1 if rr else 0
+    a.mkeys, a.mvals, a.mtile, a.mrr = sk.data_ptr(), sv.data_ptr(), st, int(rr)
     a.mbase = None if base is None else base.data_ptr()
 
 
@@ -480,8 +526,10 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
                                                      _lib.stream_ptr()), "alto_cast_f32_f64")
         return out
     a, _keep = _args(tensor, fdev, mode, out, tile, 1 if zero_out else 0)
-    ms = (mode_stream(tensor, mode) if planned is True and _use_mode_stream(tensor, rank, fdev[0].element_size())
-          else None)
+    npairs = (len(ms_pairs(tensor.layout.dims, mode, rank, 4))
+              if tensor.vals.dtype == torch.float32 and fdev[0].dtype == torch.float32 else 0)
+    ms = (mode_stream(tensor, mode, rank=rank, n_pairs=npairs)
+          if planned is True and _use_mode_stream(tensor, rank, fdev[0].element_size()) else None)
     if ms is not None:
         _set_stream(a, ms)
         tabs = []  # product tables: stream-ordered, released after the launch
@@ -507,7 +555,6 @@ ALTO_MS_ROW_MAJOR = 1
 # 6.47 / 6.96, 4096 -> 6.43 / 6.32 / 6.83, 8192 -> 6.45 / 6.39 / 6.87
 # (fewer boundary records, longer runs); shorter slices are slower.
 PULL_TILE = 4096
-
 
 def pull_stream(tensor: AltoTensor, mode: int):
     """The mode's row-major stream with contiguous slices (alto_mode_stream,
@@ -797,7 +844,8 @@ def mttkrp_det(tensor: AltoTensor, fdev: list, mode: int, out=None):
     a, _keep = _args(tensor, fdev, mode, fixed, DEFAULT_TILE, 1, vals=vals)
     a.out_dtype = _lib.ALTO_I64
     a.fixed_scale = scale.data_ptr()
-    ms = mode_stream(tensor, mode, vals) if _use_mode_stream(tensor, rank, fdev[0].element_size()) else None
+    ms = (mode_stream(tensor, mode, vals, rank=rank)
+          if _use_mode_stream(tensor, rank, fdev[0].element_size()) else None)
     if ms is not None:
         _set_stream(a, ms)
     else:

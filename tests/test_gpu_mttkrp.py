@@ -271,7 +271,7 @@ class TestStreamKernel:
                 a = mttkrp_stream(alto, fdev, mode, out_dtype=torch.float32, planned=variant).double().cpu().numpy()
                 assert rel_error(a, b) <= 1e-6, variant
 
-    @pytest.mark.parametrize("rrobin", [0, 1])
+    @pytest.mark.parametrize("rrobin", [0, 1, 3])
     @pytest.mark.parametrize("order", [0, 1])
     @pytest.mark.parametrize("cfg", [2, "wide", 4])
     def test_mode_stream_layout(self, at, monkeypatch, cfg, order, rrobin):
@@ -306,6 +306,12 @@ class TestStreamKernel:
             KW = 1 if delta else W
             sk = sk.cpu().numpy().view(np.uint64).reshape(-1, KW)
             sv = sv.cpu().numpy()
+            if rr == 2:
+                # blocked: sorted element k*gpw+s of a warp step is stored at s*u+k (group s
+                # takes sorted positions s, s+gpw, ...): back to sorted order
+                u, gpw = mk.ms_block(len(dims), 16, 0 if sv.dtype == np.float32 else 1, 0)
+                bperm = np.arange(sk.shape[0]).reshape(-1, gpw, u).transpose(0, 2, 1).reshape(-1)
+                sk, sv = sk[bperm], sv[bperm]
             forder = [n for n in range(len(dims)) if n != mode] + [mode]
             cur, fields = 0, {}
             for n in forder:
@@ -320,8 +326,11 @@ class TestStreamKernel:
                 base = base.cpu().numpy()
                 inc = ((sk[:, 0] >> np.uint64(fields[mode][1])) & np.uint64((1 << fields[mode][2]) - 1)).astype(np.int64)
                 nt = (alto.nnz + T - 1) // T
-                g = inc[:nt * T].reshape(nt, T // 8, 8) if rr else inc[:nt * T].reshape(nt, T // 8, 8)
-                rows_all = (np.cumsum(g, axis=1) + base[:nt * 8].reshape(nt, 1, 8)).reshape(-1)
+                gpw = 8
+                if rr == 2:
+                    gpw = mk.ms_block(len(dims), 16, 0 if sv.dtype == np.float32 else 1, 0)[1]
+                g = inc[:nt * T].reshape(nt, T // gpw, gpw)
+                rows_all = (np.cumsum(g, axis=1) + base[:nt * gpw].reshape(nt, 1, gpw)).reshape(-1)
             hs = mk.hot_slots(alto, mode)
             hot_rows = set() if hs is None else set(hs[1][:hs[2]].cpu().numpy().tolist())
             ch = T // 8

@@ -7,7 +7,7 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_probe \
 //        tools/gather_probe.cu -L/usr/local/cuda/lib64/stubs -lcuda
-//   ./gather_probe <variant: ldg|tma> <skew: 0 uniform, 1 skewed> [box_rows]
+//   ./gather_probe <variant: ldg|tex4|tex2|tex1|tma> <skew: 0 uniform, 1 skewed> [box_rows] [table rows]
 //
 // Not part of the product: a measurement tool for DESIGN.md §4.
 #include <cuda.h>
@@ -42,6 +42,37 @@ __global__ void __launch_bounds__(THREADS, 3) ldg_kernel(const float* __restrict
       float4 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(F + (size_t)r[u] * R) + gl);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc.x + acc.y + acc.z + acc.w;
+}
+
+// (C) texture path: the same rows fetched with tex1Dfetch<float4> from a linear
+// texture object (the TEX data pipe of the L1), all of them (TEXF = 4) or
+// TEXF of every 4 row gathers with the others on LDG (do the two pipes add up?).
+template <int TEXF>
+__global__ void __launch_bounds__(THREADS, 3) tex_kernel(cudaTextureObject_t tex, const float* __restrict__ F,
+                                                         const unsigned* __restrict__ idx, long long n, float* out) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, gl = lane & 3;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (long long c = w0 * 256; c < n; c += nw * 256) {
+#pragma unroll 1
+    for (int j = 0; j < 256; j += 32) {
+      unsigned r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = __ldg(idx + c + j + u * 8 + g);
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (u < TEXF)
+          v[u] = tex1Dfetch<float4>(tex, static_cast<int>(r[u] * 4 + gl));
+        else
+          v[u] = __ldg(reinterpret_cast<const float4*>(F + (size_t)r[u] * R) + gl);
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
     }
@@ -120,7 +151,9 @@ int main(int argc, char** argv) {
   const char* variant = argc > 1 ? argv[1] : "ldg";
   const int skew = argc > 2 ? atoi(argv[2]) : 0;
   const int box_rows = argc > 3 ? atoi(argv[3]) : 1;
-  const long long rows_tab = 200000;       // cfg2 mode-0 factor: 12.8 MB (L2 resident)
+  // table rows: default = cfg2 mode-0 factor, 12.8 MB (L2 resident); 20000000 = cfg5 mode-1 factor,
+  // 1.28 GB (random 64-byte rows from DRAM)
+  const long long rows_tab = argc > 4 ? atoll(argv[4]) : 200000;
   const long long n = 100000000;           // 2 gathered rows x 50M elements (cfg2, one mode)
   std::vector<float> hF(rows_tab * R);
   for (size_t i = 0; i < hF.size(); ++i) hF[i] = (float)((i * 2654435761u) % 1000) * 1e-3f;
@@ -154,9 +187,26 @@ int main(int argc, char** argv) {
     if (r) return 1;
     CK(cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * STAGES * STAGE_BYTES));
   }
+  cudaTextureObject_t tex = 0;
+  if (strncmp(variant, "tex", 3) == 0) {
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = F;
+    rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+    rd.res.linear.sizeInBytes = hF.size() * 4;
+    cudaTextureDesc td{};
+    td.readMode = cudaReadModeElementType;
+    CK(cudaCreateTextureObject(&tex, &rd, &td, nullptr));
+  }
   cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
   auto launch = [&]() {
-    if (strcmp(variant, "tma") == 0)
+    if (strcmp(variant, "tex4") == 0)
+      tex_kernel<4><<<blocks, THREADS>>>(tex, F, I, n, out);
+    else if (strcmp(variant, "tex2") == 0)
+      tex_kernel<2><<<blocks, THREADS>>>(tex, F, I, n, out);
+    else if (strcmp(variant, "tex1") == 0)
+      tex_kernel<1><<<blocks, THREADS>>>(tex, F, I, n, out);
+    else if (strcmp(variant, "tma") == 0)
       tma_kernel<<<blocks, THREADS, 8 * STAGES * STAGE_BYTES>>>(tm, I, n, out, box_rows);
     else
       ldg_kernel<<<blocks, THREADS>>>(F, I, n, out);
@@ -170,7 +220,7 @@ int main(int argc, char** argv) {
   std::vector<float> ho((size_t)blocks * THREADS);
   CK(cudaMemcpy(ho.data(), out, ho.size() * 4, cudaMemcpyDeviceToHost));
   double s = 0; for (float v : ho) s += v;
-  printf("variant=%s skew=%d box_rows=%d rows=%lld best_ms=%.4f Grows/s=%.1f sum_rel_err=%.2e\n", variant, skew, box_rows, n, best,
+  printf("variant=%s skew=%d box_rows=%d table_rows=%lld rows=%lld best_ms=%.4f Grows/s=%.1f sum_rel_err=%.2e\n", variant, skew, box_rows, rows_tab, n, best,
          n / (best * 1e-3) / 1e9, std::fabs(s - ref) / ref);
   return 0;
 }
