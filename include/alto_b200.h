@@ -306,20 +306,9 @@ int alto_coalesce(const int64_t* coords, const double* values, int64_t m, int32_
                   int64_t* out_coords, double* out_values, int64_t* d_count, void* ws, size_t ws_bytes,
                   void* stream);
 
-/* Streaming-kernel tuning switches (alto_mttkrp_args.flags). */
-#define ALTO_STREAM_WARP_AGG 1   /* warp-aggregate in-tile sort atomics */
-#define ALTO_STREAM_FULL_BINS 2  /* scan all sort bins instead of the tile span */
-#define ALTO_STREAM_CTA_TILES 4  /* CTA-wide 1024-element tiles (cp.async staged)
-                                    instead of warp-autonomous 128-element tiles */
+/* Streaming-kernel switches (alto_mttkrp_args.flags). */
 #define ALTO_STREAM_GENERIC 128  /* bypass the specialised (order 3-5, rank 16/32) kernels */
-#define ALTO_STREAM_TUNE_MINB2 256  /* tuning: planned kernel: 2 CTAs/SM launch bounds (default 3) */
-#define ALTO_STREAM_TUNE_U4 512     /* tuning: planned kernel: 4 elements in flight per group (default 2) */
 #define ALTO_STREAM_MS_L2_NORMAL 2048 /* tuning: mode-stream loads without the L2 evict_first policy */
-/* Ablation switches for profiling only (results are wrong when set). */
-#define ALTO_STREAM_DBG_NO_RED 8
-#define ALTO_STREAM_DBG_NO_GATHER 16
-#define ALTO_STREAM_DBG_NO_HOT 32
-#define ALTO_STREAM_DBG_NO_SORT 64
 
 /* Build the hot-row plan of one mode from its row pointer (alto_row_index):
  * rows with more than `tau` elements get slots (at most hmax);

@@ -378,7 +378,7 @@ int try_mstream(const DevLayout& d, const StreamParams& P, cudaStream_t s);
 
 template <int W, typename V, typename O>
 int try_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cudaStream_t s) {
-  if (P.flags & (ALTO_STREAM_CTA_TILES | ALTO_STREAM_GENERIC)) return ALTO_EUNSUPPORTED;
+  if (P.flags & ALTO_STREAM_GENERIC) return ALTO_EUNSUPPORTED;
   if (P.mkeys) {
     // a mode stream pins the kernel (its hot copies are float64 for float32 output)
     const int st = try_mstream<W, V, O>(d, P, s);
@@ -395,13 +395,6 @@ int try_fast(const DevLayout& d, const uint64_t* tab, const StreamParams& P, cud
   for (int n = 0; n < d.order; ++n)
     if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
   if (P.rank == 16) {
-    if constexpr (W == 1 && sizeof(V) == 4 && sizeof(O) == 4) {
-      // tuning variants (ALTO_STREAM_TUNE_* flags), cfg2 shape only
-      if (d.order == 3 && (P.flags & ALTO_STREAM_TUNE_MINB2) && (P.flags & ALTO_STREAM_TUNE_U4))
-        return launch_fast<W, V, O, 3, 16, 2, 4>(d, tab, P, s);
-      if (d.order == 3 && (P.flags & ALTO_STREAM_TUNE_MINB2)) return launch_fast<W, V, O, 3, 16, 2, 2>(d, tab, P, s);
-      if (d.order == 3 && (P.flags & ALTO_STREAM_TUNE_U4)) return launch_fast<W, V, O, 3, 16, 3, 4>(d, tab, P, s);
-    }
     if (d.order == 3) return launch_fast<W, V, O, 3, 16>(d, tab, P, s);
     if (d.order == 4) return launch_fast<W, V, O, 4, 16>(d, tab, P, s);
     if (d.order == 5) return launch_fast<W, V, O, 5, 16>(d, tab, P, s);
@@ -643,7 +636,7 @@ int launch_planned(const DevLayout& d, const StreamParams& P, const uint64_t* pa
 template <int W, typename V, typename O>
 int try_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packed, const unsigned char* pos,
                 cudaStream_t s) {
-  if (!packed || !pos || (P.flags & (ALTO_STREAM_CTA_TILES | ALTO_STREAM_GENERIC))) return ALTO_EUNSUPPORTED;
+  if (!packed || !pos || (P.flags & ALTO_STREAM_GENERIC)) return ALTO_EUNSUPPORTED;
   long long maxdim = 0;
   for (int n = 0; n < d.order; ++n) maxdim = std::max(maxdim, d.dims[n]);
   if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
