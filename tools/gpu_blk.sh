@@ -1,8 +1,8 @@
 cd $GRAFT_REPO_ROOT; export PYTHONPATH=$GRAFT_REPO_ROOT
-make -C oracle >/dev/null
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
-timeout 900 python -m pytest tests/test_gpu_smoke.py tests/test_gpu_sort.py tests/test_gpu_layout.py tests/test_gpu_format.py tests/test_coo.py tests/test_gpu_mttkrp.py -q > gpurun_out/t_s.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/t_s.log
-for ot in 512 256; do
-for c in 5 2; do ALTO_SORT_OT=$ot timeout 600 python bench.py --config $c --skip-paths --skip-cpals --skip-cpu --steps 3 --e2e-steps 1 > gpurun_out/bq$c.log 2>&1; echo "ot=$ot bench$c rc=$?"; python -c "
-import json; d=json.loads([l for l in open('gpurun_out/bq$c.log') if l.startswith('{')][-1]); print('cfg$c build_ms', d['build_ms'], 'plans', d['plans'], 'value', d['value'], d['roofline']['frac'])"; done
+timeout 600 python tools/reuse_stats.py 5 > gpurun_out/reuse_stats_cfg5.jsonl 2> gpurun_out/reuse.err; echo "reuse rc=$?"; cat gpurun_out/reuse_stats_cfg5.jsonl
+B="python bench.py --steps 1 --warmup 3 --skip-cpu --skip-cpals --e2e-steps 1 --skip-paths"
+for c in 3 4; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:mstream_blk_kernel --launch-skip 8 -c 5 -o gpurun_out/r02e_cfg${c}_mstream_blk -f $B --config $c > gpurun_out/ncu_b$c.log 2>&1; echo "ncu cfg$c rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r02e_launches_cfg$c.csv python bench.py --steps 2 --warmup 3 --skip-cpu --skip-cpals --skip-paths --e2e-steps 1 --config $c > gpurun_out/ncu_l$c.log 2>&1; echo "launches cfg$c rc=$?"
 done
+ls -la gpurun_out/*.ncu-rep
