@@ -227,7 +227,7 @@ def traffic_from_profile(cfg_id: int):
         rows = json.load(open(files[-1]))
         vals = []
         for r in rows:
-            if "mstream_kernel" in r["kernel"]:
+            if "mstream_kernel" in r["kernel"] or "mstream_blk_kernel" in r["kernel"]:
                 rd = float(r["dram__bytes_read.sum"]["value"])
                 wr = float(r["dram__bytes_write.sum"]["value"])
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -458,7 +458,12 @@ def run_b200(args):
     achieved = tot_b / (sum(mode_ms) * 1e-3) / 1e9
     ms_used = all(any(k[0] == "mstream" and k[1] == n and v for k, v in alto._cache.items() if isinstance(k, tuple))
                   for n in range(N))
-    kernel_name = "alto::mstream_kernel (alto_mstream.cuh)" if ms_used else "alto::planned_kernel (alto_fast.cuh)"
+    blocked = ms_used and alto.vals.dtype == torch.float32 and mk.MS_RR == 2 and (R == 32 or N >= 4)
+    kernel_name = (("alto::mstream_blk_kernel (alto_mstream.cuh)" if blocked else "alto::mstream_kernel (alto_mstream.cuh)")
+                   if ms_used else "alto::planned_kernel (alto_fast.cuh)")
+    # row gathers per element and mode: N-1 inputs, one fewer per paired input mode
+    gathers_per_element = [N - 1 - (len(mk.ms_pairs(dims, n, R, 4)) if ms_used and alto.vals.dtype == torch.float32
+                                    else 0) for n in range(N)]
     launches_per_step = 0
     for n in range(N):
         launches_per_step += 1
@@ -633,7 +638,14 @@ def run_b200(args):
                          "bytes_alg_per_launch": tot_b / N, "kernel": kernel_name,
                          "timing": "per-mode CUDA events around the whole MTTKRP call (output zeroing, "
                                    "mode-stream kernel, hot-row reduction)",
-                         "per_mode": per_mode},
+                         "per_mode": per_mode,
+                         # the access pattern's own ceiling: one factor-row gather per
+                         # element and gathered input; tools/gather_probe.cu measures 164-167 G rows/s for
+                         # 64-byte rows out of L2 and 40 G rows/s out of HBM (profiles/r02e_gather_probe.txt)
+                         "row_gathers_per_s": sum(M * gathers_per_element[n] for n in range(N))
+                                              / (sum(mode_ms) * 1e-3),
+                         "row_gather_ceiling_per_s": {"l2_resident_64B_rows": 165e9, "hbm_64B_rows": 40e9,
+                                                      "source": "profiles/r02e_gather_probe.txt"}},
             "paths": paths,
             "plans": plans,
             "e2e": {"value": N * nnz_total / (e2e_ms * 1e-3), "unit": "nnz/s", "h2d_bytes_per_step": h2d,

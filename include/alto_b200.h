@@ -203,6 +203,13 @@ typedef struct alto_mttkrp_args {
   /* Delta mode stream (alto_mode_stream with ALTO_MS_DELTA): the row of each
    * lane group's first element (ntiles * 8 int32); NULL for plain streams. */
   const int32_t* mbase;
+  /* L2 residency of gathered factor rows (mode-stream kernel, float32
+   * factors): the first l2_hot_bytes[n] bytes of mode n's factor — its most
+   * referenced rows when rows are numbered by popularity — are gathered with
+   * an L2 evict_last policy and the rest of it with evict_first, so the
+   * re-used head stays cached while the stream, the tail rows and the output
+   * rows pass through (0 = default policy). */
+  uint32_t l2_hot_bytes[ALTO_MAX_ORDER];
 } alto_mttkrp_args;
 
 /* Row-wise (Khatri-Rao) product table of two factors for paired input modes:

@@ -68,6 +68,7 @@ class CMttkrpArgs(Structure):
         ("pair_b", c_int32 * 2),
         ("pair_tab", c_void_p * 2),
         ("mbase", c_void_p),
+        ("l2_hot_bytes", ctypes.c_uint32 * ALTO_MAX_ORDER),
     ]
 
 

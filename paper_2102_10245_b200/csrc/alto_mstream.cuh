@@ -165,7 +165,11 @@ struct MStream {
   const int* base;       // delta stream: row of every lane group's first element (ntiles x 8)
 };
 
-template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, int NV = N - 1, bool DELTA = false>
+// L2P: factor rows are gathered with a per-table L2 range policy (the
+// table's first l2_hot bytes evict_last, the rest evict_first) and output
+// rows merged with evict_first (alto_mttkrp_args.l2_hot_bytes).
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, int NV = N - 1, bool DELTA = false,
+          bool L2P = false>
 __global__ void __launch_bounds__(kTileThreads, MINB)
 mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStream S,
                const __grid_constant__ StreamParams P) {
@@ -225,6 +229,15 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
   O* __restrict__ hot_buf = static_cast<O*>(P.hot_buf);
   const unsigned hotmask = hot_code ? HOTF : 0u;  // stream flags are ignored without a hot plan
   const unsigned long long pol = stream_policy(!(P.flags & ALTO_STREAM_MS_L2_NORMAL));
+  unsigned long long gpol[L2P ? NIN : 1];
+  if constexpr (L2P) {
+    static_assert(!PAIR && sizeof(F) == 4 && std::is_same<O, float>::value, "L2 policies: unpaired float32 kernels");
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      const int n = k < mode ? k : k + 1;
+      gpol[k] = range_policy(P.factors[n], P.l2_hot[n], P.l2_tab[n]);
+    }
+  }
 
   const long long ntiles = (P.m + T - 1) / T;
   const long long gw0 = static_cast<long long>(blockIdx.x) * (kTileThreads / 32) + warp;
@@ -249,7 +262,10 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
         } else {
           base = out + static_cast<long long>(cur) * R;
         }
-        merge_row<O, A, G, R>(base, acc, gl, qmask, lane, fixed_scale);
+        if constexpr (L2P)
+          red_f32x4_pol(reinterpret_cast<float*>(base) + 4 * gl, acc, pol);  // output rows pass through the L2
+        else
+          merge_row<O, A, G, R>(base, acc, gl, qmask, lane, fixed_scale);
       };
       // loop trip count is uniform across the warp's groups except in the
       // final partial tile; inactive groups keep their lanes converged
@@ -329,7 +345,12 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
 #pragma unroll
               for (int k = 0; k < NIN; ++k) {
                 const unsigned off = __shfl_sync(0xffffffffu, moff[k], gbase + u);
-                if (tg[u] != 0xffffffffu) g[u][k] = gather_off<F>(fin_lane[k], off);
+                if (tg[u] != 0xffffffffu) {
+                  if constexpr (L2P)
+                    g[u][k] = gather_off_pol(fin_lane[k], off, gpol[k]);
+                  else
+                    g[u][k] = gather_off<F>(fin_lane[k], off);
+                }
               }
             }
           }
@@ -554,8 +575,14 @@ constexpr int ms_u() {
 }
 
 template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = ms_u<N, R, V, 32>(), int NV = N - 1,
-          bool DELTA = false>
+          bool DELTA = false, bool L2P = false>
 int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, cudaStream_t s) {
+  if constexpr (!L2P && N == 3 && R == 16 && NV == 2 && sizeof(V) == 4 && std::is_same<O, float>::value) {
+    // L2 residency policies requested for an input factor (order 3, rank 16, float32)
+    bool want = false;
+    for (int n = 0; n < 3; ++n) want = want || (n != P.mode && P.l2_hot[n] > 0);
+    if (want && S.rr != 2) return launch_mstream<W, V, O, N, R, MINB, U, NV, DELTA, true>(d, S, P, s);
+  }
   if (S.rr == 2) {
     // blocked stream (ALTO_MS_BLOCKED): broadcast vector loads, redundant decode, no shuffles
     constexpr int GPW = 32 / (R / 4);
@@ -593,7 +620,7 @@ int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, 
     ALTO_LAUNCH_CHECK("alto_mttkrp(blocked mode stream)");
     return ALTO_OK;
   }
-  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, NV, DELTA>;
+  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, NV, DELTA, L2P>;
   static int cached_bps = 0;
   if (!cached_bps) {
     int b = 1;

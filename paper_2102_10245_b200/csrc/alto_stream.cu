@@ -169,6 +169,12 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.mtile = a->mtile;
   P.mrr = a->mrr;
   P.mbase = a->mkeys ? a->mbase : nullptr;
+  for (int n = 0; n < ALTO_MAX_ORDER; ++n) {
+    const bool on = n < d.order && a->factor_dtype == ALTO_F32 && a->l2_hot_bytes[n] > 0;
+    const unsigned long long tb = on ? static_cast<unsigned long long>(d.dims[n]) * a->rank * 4ull : 0ull;
+    P.l2_tab[n] = static_cast<unsigned>(std::min<unsigned long long>(tb, 0xFFFFFFFFull));
+    P.l2_hot[n] = on ? std::min(a->l2_hot_bytes[n], P.l2_tab[n]) : 0u;
+  }
   P.n_pairs = (a->mkeys && a->out_dtype != ALTO_I64) ? std::max(0, std::min(a->n_pairs, 2)) : 0;
   ALTO_REQUIRE(a->n_pairs <= 2, "at most 2 paired input modes");
   for (int i = 0; i < 2; ++i) {

@@ -61,7 +61,9 @@ struct StreamParams {
   int n_pairs;                // paired input modes (mode stream): count,
   int pair_a[2], pair_b[2];   //   modes,
   const void* pair_tab[2];    //   row-wise product tables (alto_krp_pair)
-  const double* fixed_scale;  // deterministic mode: device scalar, int64 output = round(x * scale)  // tuning switches (ALTO_STREAM_* bits in alto_b200.h)
+  const double* fixed_scale;  // deterministic mode: device scalar, int64 output = round(x * scale)
+  unsigned l2_hot[ALTO_MAX_ORDER];  // per mode: leading bytes of its factor gathered with L2 evict_last (0 = no policy)
+  unsigned l2_tab[ALTO_MAX_ORDER];  //   and the factor's size in bytes
 };
 
 template <typename V, typename F>
@@ -115,6 +117,30 @@ __device__ __forceinline__ V4<F> gather_off(const char* base, unsigned off) {
     o.v[0] = a.x; o.v[1] = a.y; o.v[2] = b.x; o.v[3] = b.y;
   }
   return o;
+}
+
+// L2 policy per gathered table: the first `hot` bytes evict_last (the most
+// referenced rows when rows are numbered by popularity), the rest evict_first.
+__device__ __forceinline__ unsigned long long range_policy(const void* tab, unsigned hot, unsigned total) {
+  unsigned long long p;
+  asm volatile("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+               : "=l"(p)
+               : "l"(tab), "r"(hot), "r"(total));
+  return p;
+}
+
+__device__ __forceinline__ V4<float> gather_off_pol(const char* base, unsigned off, unsigned long long pol) {
+  V4<float> o;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(o.v[0]), "=f"(o.v[1]), "=f"(o.v[2]), "=f"(o.v[3])
+      : "l"(base + off), "l"(pol));
+  return o;
+}
+
+__device__ __forceinline__ void red_f32x4_pol(float* p, const float (&acc)[4], unsigned long long pol) {
+  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(acc[0]), "f"(acc[1]),
+               "f"(acc[2]), "f"(acc[3]), "l"(pol)
+               : "memory");
 }
 
 template <int NMAX>

@@ -411,6 +411,30 @@ def mode_stream(tensor: AltoTensor, mode: int, vals=None, rank: int = 16, n_pair
     return hit or None
 
 
+# L2 residency budget (MB) for the gathered factors of the mode-stream kernel
+# on tensors whose factors exceed the L2 (alto_mttkrp_args.l2_hot_bytes): the
+# budget is split over the input modes (small factors whole, the rest evenly);
+# rows must be numbered by popularity for the leading bytes to be the hot ones
+# (the synthetic configs are).  0 = default L2 policy.
+MS_L2_HOT_MB = 0
+
+
+def l2_hot_bytes(dims, mode: int, rank: int, fbytes: int = 4, budget_mb: float | None = None):
+    """Per-mode leading bytes gathered with the L2 evict_last policy."""
+    budget = int((MS_L2_HOT_MB if budget_mb is None else budget_mb) * (1 << 20))
+    out = [0] * len(dims)
+    ins = sorted((n for n in range(len(dims)) if n != mode), key=lambda n: dims[n])
+    sizes = {n: dims[n] * rank * fbytes for n in ins}
+    if budget <= 0 or sum(sizes.values()) <= budget:
+        return out  # everything fits anyway: leave the default policy
+    left = budget
+    for i, n in enumerate(ins):
+        share = left // (len(ins) - i)
+        out[n] = int(min(sizes[n], share, (1 << 32) - 1))
+        left -= out[n]
+    return out
+
+
 def _set_stream(a, ms) -> None:
     sk, sv, st, rr, base = ms
     a.mkeys, a.mvals, a.mtile, a.mrr = sk.data_ptr(), sv.data_ptr(), st, int(rr)
@@ -534,6 +558,9 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
         _set_stream(a, ms)
         tabs = []  # product tables: stream-ordered, released after the launch
         _set_pairs(a, tensor, fdev, mode, tabs)
+        if MS_L2_HOT_MB and fdev[0].dtype == torch.float32 and out.dtype == torch.float32:
+            for n, b in enumerate(l2_hot_bytes(tensor.layout.dims, mode, rank, 4)):
+                a.l2_hot_bytes[n] = b
     elif planned and tensor.nnz > 0 and rank in (16, 32) and 3 <= tensor.layout.order <= 5 \
             and max(tensor.layout.bits) <= 31:
         # the single ALTO-order copy: packed keys + per-mode sub-tile order

@@ -19,7 +19,7 @@ import subprocess
 import sys
 
 
-STEP_KERNELS = ("mstream_kernel<", "hot_reduce_rows_kernel<float>")
+STEP_KERNELS = ("mstream_kernel<", "mstream_blk_kernel<", "hot_reduce_rows_kernel<float>", "krp_pair_kernel")
 
 
 def launches(path: str, out: str) -> None:
