@@ -3,8 +3,9 @@
 //
 // Replaces np.lexsort over the index words with last word primary and the
 // co-permutation of values (format.py:79-82, :94-97).  Because keys occupy
-// only bits [0, total_bits), exactly ceil(total_bits/8) 8-bit digit passes
-// are run (4/7/9/6/9 passes for BASELINE cfg1..cfg5).
+// only bits [0, total_bits), exactly ceil(total_bits/9) 9-bit digit passes
+// are run by the one-sweep path (ceil(total_bits/8) 8-bit passes by the
+// three-kernel fallback for m >= 2^30).
 //
 // One pass = three stream-ordered kernels:
 //   1. radix_hist   : per-tile digit histogram -> counts[digit * ntiles + tile]
@@ -252,36 +253,56 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(const uint64_t* __
 // --- one-sweep passes (decoupled look-back) ------------------------------------
 // Used when m < 2^30: one histogram kernel for every pass up front
 // (onesweep_hist + onesweep_scan: global digit bases), then per pass a single
-// kernel that reads each key/payload once and writes it once.  A CTA claims
-// the next tile in order (atomic counter), ranks it like radix_scatter,
-// publishes its per-digit counts (flag AGGREGATE), looks back over earlier
-// tiles until it finds an inclusive prefix (flag PREFIX), publishes its own,
-// and scatters the tile (staged digit-sorted in shared memory, coalesced
-// runs).  Tiles are claimed in order, so every tile a CTA waits on belongs to
-// a CTA that is already running.
+// kernel that reads each key/payload once and writes it once.  Digits are 9
+// bits wide (512 bins = one per thread of the 512-thread CTA: cfg5's 71 key
+// bits take 8 passes instead of 9, and an even pass count ends in the caller's
+// buffer).  A CTA claims the next 4096-key tile in order (atomic counter),
+// ranks it like radix_scatter, publishes its per-digit counts at once (flag
+// AGGREGATE), stages the tile digit-sorted in shared memory, then looks back
+// over earlier tiles until it finds an inclusive prefix (flag PREFIX) —
+// their aggregates were published before their own staging, so the walk
+// rarely spins — publishes its own prefix and writes the tile out in
+// coalesced runs.  Tiles are claimed in order, so every tile a CTA waits on
+// belongs to a CTA that is already running.
 constexpr int kMaxPasses = 16;
 constexpr int kOnesweepThreads = 512;  // one-sweep CTA: 4096-key tiles
+constexpr int kOneBits = 9;            // one-sweep digit width: 512 bins, one per thread of the CTA
+constexpr int kOneBins = 1 << kOneBits;
+static_assert(kOneBins == kOnesweepThreads, "thread d of a one-sweep CTA owns digit d");
 constexpr unsigned kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValMask = (1u << 30) - 1u;
+
+// kOneBits-wide digit at bit `shift` (may straddle the two key words)
+template <int W>
+__device__ __forceinline__ unsigned digit9(const Key<W>& k, int shift) {
+  if constexpr (W == 1) {
+    return static_cast<unsigned>(k.w[0] >> shift) & (kOneBins - 1);
+  } else {
+    const int sh = shift & 63;
+    uint64_t v = (shift >= 64 ? k.w[1] : k.w[0]) >> sh;
+    if (shift < 64 && sh > 64 - kOneBits) v |= k.w[1] << (64 - sh);
+    return static_cast<unsigned>(v) & (kOneBins - 1);
+  }
+}
 
 template <int W>
 __global__ void __launch_bounds__(kSortThreads) onesweep_hist(const uint64_t* __restrict__ keys, long long m,
                                                               int passes, unsigned* __restrict__ ghist) {
-  __shared__ unsigned s_h[kMaxPasses * 256];
-  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) s_h[i] = 0;
+  __shared__ unsigned s_h[kMaxPasses * kOneBins];
+  for (int i = threadIdx.x; i < passes * kOneBins; i += blockDim.x) s_h[i] = 0;
   __syncthreads();
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m; i += stride) {
     const Key<W> k = load_key<W>(keys, i);
-    for (int p = 0; p < passes; ++p) atomicAdd(&s_h[p * 256 + digit_of<W>(k, 8 * p)], 1u);
+    for (int p = 0; p < passes; ++p) atomicAdd(&s_h[p * kOneBins + digit9<W>(k, kOneBits * p)], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+  for (int i = threadIdx.x; i < passes * kOneBins; i += blockDim.x)
     if (s_h[i]) atomicAdd(ghist + i, s_h[i]);
 }
 
-__global__ void __launch_bounds__(256) onesweep_scan(unsigned* __restrict__ ghist) {
+__global__ void __launch_bounds__(kOneBins) onesweep_scan(unsigned* __restrict__ ghist) {
   __shared__ unsigned s_tmp[32];
-  unsigned* h = ghist + static_cast<long long>(blockIdx.x) * 256;
+  unsigned* h = ghist + static_cast<long long>(blockIdx.x) * kOneBins;
   const unsigned v = h[threadIdx.x];
   unsigned total;
   const unsigned ex = block_exclusive_scan(v, s_tmp, &total);
@@ -297,7 +318,7 @@ __device__ __forceinline__ void st_status(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// OT threads per CTA, tile = OT * kSortItems keys; threads < 256 own one digit.
+// OT = kOneBins threads per CTA, tile = OT * kSortItems keys; thread d owns digit d.
 template <int W, int P, int OT>
 __global__ void __launch_bounds__(OT, 1024 / OT) onesweep_pass(const uint64_t* __restrict__ keys_in,
                                                               const void* __restrict__ pay_in,
@@ -306,10 +327,12 @@ __global__ void __launch_bounds__(OT, 1024 / OT) onesweep_pass(const uint64_t* _
                                                               const unsigned* __restrict__ gbase,
                                                               unsigned* __restrict__ status,
                                                               unsigned* __restrict__ tile_ctr) {
+  static_assert(OT == kOneBins, "one digit per thread");
   constexpr int NW = OT / 32, TILE = OT * kSortItems, SLICE = TILE / NW;
-  __shared__ unsigned s_warp[NW][256];
-  __shared__ unsigned s_base[256];
-  __shared__ unsigned s_dstart[256];
+  static_assert(SLICE <= 65535 && TILE <= 65535, "16-bit per-warp digit counters");
+  __shared__ unsigned short s_warp[NW][kOneBins];  // per-warp digit counts, then exclusive scan over warps
+  __shared__ unsigned s_base[kOneBins];
+  __shared__ unsigned short s_dstart[kOneBins];
   __shared__ unsigned s_scan[32];
   __shared__ unsigned s_tile;
   extern __shared__ __align__(16) unsigned char s_dyn[];  // digit-sorted tile: keys, then payload
@@ -320,7 +343,7 @@ __global__ void __launch_bounds__(OT, 1024 / OT) onesweep_pass(const uint64_t* _
   (void)s_pay64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int i = threadIdx.x; i < NW * 256; i += blockDim.x) (&s_warp[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < NW * kOneBins / 2; i += blockDim.x) reinterpret_cast<unsigned*>(&s_warp[0][0])[i] = 0;
   __syncthreads();
   const long long tile = s_tile;
   const long long base = tile * TILE + static_cast<long long>(warp) * SLICE;
@@ -332,7 +355,7 @@ __global__ void __launch_bounds__(OT, 1024 / OT) onesweep_pass(const uint64_t* _
   for (int j = 0; j < kSortItems; ++j) {
     const long long i = base + j * 32 + lane;
     const bool valid = i < m;
-    unsigned d = 0x100u + lane;  // invalid lanes: singleton groups
+    unsigned d = kOneBins + lane;  // invalid lanes: singleton groups
     k0[j] = 0;
     k1[j] = 0;
     pv[j] = 0;
@@ -342,64 +365,45 @@ __global__ void __launch_bounds__(OT, 1024 / OT) onesweep_pass(const uint64_t* _
       if constexpr (W == 2) k1[j] = kk.w[1];
       if constexpr (P == 4) pv[j] = static_cast<const unsigned*>(pay_in)[i];
       if constexpr (P == 8) pv[j] = static_cast<const uint64_t*>(pay_in)[i];
-      d = digit_of<W>(kk, shift);
+      d = digit9<W>(kk, shift);
     }
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const unsigned r = __popc(peers & lt_mask);
     unsigned prior = 0;
     if (valid) prior = s_warp[warp][d];
     __syncwarp();
-    if (valid && r == 0) s_warp[warp][d] = prior + __popc(peers);
+    if (valid && r == 0) s_warp[warp][d] = static_cast<unsigned short>(prior + __popc(peers));
     __syncwarp();
-    rd[j] = ((prior + r) << 8) | (d & 0xffu);
+    rd[j] = ((prior + r) << kOneBits) | (d & (kOneBins - 1));
   }
   __syncthreads();
-  // per-digit exclusive scan over warps (stable order of warps) and the
-  // tile-local exclusive scan over digits; thread d < 256 owns digit d
+  // per-digit exclusive scan over warps (stable order of warps); thread d owns
+  // digit d and publishes the tile's count for it at once (AGGREGATE), so the
+  // later tiles' look-back does not wait for this tile's scatter
   const int d = threadIdx.x;
   unsigned run = 0;
-  if (d < 256) {
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const unsigned c = s_warp[w][d];
-      s_warp[w][d] = run;
-      run += c;
-    }
+  for (int w = 0; w < NW; ++w) {
+    const unsigned c = s_warp[w][d];
+    s_warp[w][d] = static_cast<unsigned short>(run);
+    run += c;
   }
+  unsigned* st = status + tile * kOneBins + d;
+  st_status(st, (tile == 0 ? kFlagPrefix : kFlagAgg) | run);
   {
+    // tile-local exclusive scan over digits
     unsigned total;
     const unsigned ds = block_exclusive_scan(run, s_scan, &total);
-    if (d < 256) s_dstart[d] = ds;
-  }
-  if (d < 256) {
-    // decoupled look-back over the earlier tiles for digit d
-    unsigned* st = status + tile * 256 + d;
-    unsigned excl = 0;
-    if (tile == 0) {
-      st_status(st, kFlagPrefix | run);
-    } else {
-      st_status(st, kFlagAgg | run);
-      const unsigned* q = st - 256;
-      while (true) {
-        unsigned v;
-        do {
-          v = ld_status(q);
-        } while ((v & ~kValMask) == 0u);
-        excl += v & kValMask;
-        if ((v & ~kValMask) == kFlagPrefix) break;
-        q -= 256;
-      }
-      st_status(st, kFlagPrefix | (excl + run));
-    }
-    s_base[d] = gbase[d] + excl;
+    s_dstart[d] = static_cast<unsigned short>(ds);
   }
   __syncthreads();
+  // stage the tile digit-sorted in shared memory (independent of the look-back)
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const long long i = base + j * 32 + lane;
     if (i < m) {
-      const unsigned d = rd[j] & 0xffu;
-      const unsigned lp = s_dstart[d] + s_warp[warp][d] + (rd[j] >> 8);
+      const unsigned dd = rd[j] & (kOneBins - 1);
+      const unsigned lp = s_dstart[dd] + s_warp[warp][dd] + (rd[j] >> kOneBits);
       if constexpr (W == 1) {
         s_keys[lp] = k0[j];
       } else {
@@ -409,6 +413,25 @@ __global__ void __launch_bounds__(OT, 1024 / OT) onesweep_pass(const uint64_t* _
       if constexpr (P == 4) s_pay32[lp] = static_cast<unsigned>(pv[j]);
       if constexpr (P == 8) s_pay64[lp] = pv[j];
     }
+  }
+  {
+    // decoupled look-back over the earlier tiles for digit d (their
+    // aggregates were published before their scatter, so this rarely spins)
+    unsigned excl = 0;
+    if (tile > 0) {
+      const unsigned* q = st - kOneBins;
+      while (true) {
+        unsigned v;
+        do {
+          v = ld_status(q);
+        } while ((v & ~kValMask) == 0u);
+        excl += v & kValMask;
+        if ((v & ~kValMask) == kFlagPrefix) break;
+        q -= kOneBins;
+      }
+      st_status(st, kFlagPrefix | (excl + run));
+    }
+    s_base[d] = gbase[d] + excl;
   }
   __syncthreads();
   const int cnt = static_cast<int>(min(static_cast<long long>(TILE), m - tile * TILE));
@@ -420,8 +443,8 @@ __global__ void __launch_bounds__(OT, 1024 / OT) onesweep_pass(const uint64_t* _
       key.w[0] = s_keys[2 * lp];
       key.w[1] = s_keys[2 * lp + 1];
     }
-    const unsigned d = digit_of<W>(key, shift);
-    const long long dst = static_cast<long long>(s_base[d]) + (lp - s_dstart[d]);
+    const unsigned dd = digit9<W>(key, shift);
+    const long long dst = static_cast<long long>(s_base[dd]) + (lp - s_dstart[dd]);
     store_key<W>(keys_out, dst, key);
     if constexpr (P == 4) static_cast<unsigned*>(pay_out)[dst] = s_pay32[lp];
     if constexpr (P == 8) static_cast<uint64_t*>(pay_out)[dst] = s_pay64[lp];
@@ -452,7 +475,7 @@ struct SortWs {
   void* pay_alt;
   unsigned* counts;   // per (digit, tile) counts; one-sweep: per (tile, digit) status words
   unsigned* partial;
-  unsigned* ghist;    // one-sweep: kMaxPasses x 256 digit bases + kMaxPasses tile counters
+  unsigned* ghist;    // one-sweep: kMaxPasses x kOneBins digit bases + kMaxPasses tile counters
   size_t bytes;
 };
 
@@ -461,7 +484,7 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 static SortWs carve(void* base, long long m, int W, int P) {
   SortWs w{};
   const long long ntiles = (m + kSortTile - 1) / kSortTile;
-  const long long ncounts = 256 * ntiles;
+  const long long ncounts = 256 * ntiles + 256;  // one-sweep: kOneBins status words per 4096-key tile
   const long long nparts = (ncounts + kScanChunk - 1) / kScanChunk;
   size_t off = 0;
   char* b = static_cast<char*>(base);
@@ -474,7 +497,7 @@ static SortWs carve(void* base, long long m, int W, int P) {
   w.partial = reinterpret_cast<unsigned*>(b ? b + off : nullptr);
   off += align256(static_cast<size_t>(nparts + 1) * 4);
   w.ghist = reinterpret_cast<unsigned*>(b ? b + off : nullptr);
-  off += align256(static_cast<size_t>(kMaxPasses) * 257 * 4);
+  off += align256(static_cast<size_t>(kMaxPasses) * (kOneBins + 1) * 4);
   w.bytes = off;
   return w;
 }
@@ -482,7 +505,7 @@ static SortWs carve(void* base, long long m, int W, int P) {
 template <int W, int P>
 static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, const SortWs& ws, cudaStream_t s) {
   const long long ntiles = (m + kSortTile - 1) / kSortTile;
-  const long long ncounts = 256 * ntiles;
+  const long long ncounts = 256 * ntiles + 256;  // one-sweep: kOneBins status words per 4096-key tile
   const long long nparts = (ncounts + kScanChunk - 1) / kScanChunk;
   const int passes = (total_bits + 7) / 8;
   const size_t smem = static_cast<size_t>(kSortTile) * (W * 8 + P);
@@ -496,7 +519,8 @@ static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, con
   uint64_t* kout = ws.keys_alt;
   void* pin = pay;
   void* pout = ws.pay_alt;
-  if (m < (1ll << 30) && passes <= kMaxPasses) {
+  const int opasses = (total_bits + kOneBits - 1) / kOneBits;
+  if (m < (1ll << 30) && opasses <= kMaxPasses) {
     constexpr int OT = kOnesweepThreads;
     const long long otiles = (m + OT * kSortItems - 1) / (OT * kSortItems);
     const size_t osmem = static_cast<size_t>(OT) * kSortItems * (W * 8 + P);
@@ -506,14 +530,14 @@ static int sort_impl(uint64_t* keys, void* pay, long long m, int total_bits, con
                                          static_cast<int>(osmem)));
       os_attr = true;
     }
-    unsigned* ctr = ws.ghist + kMaxPasses * 256;
-    ALTO_CUDA_TRY(cudaMemsetAsync(ws.ghist, 0, static_cast<size_t>(kMaxPasses) * 257 * 4, s));
-    onesweep_hist<W><<<grid_for(m, kSortThreads, kSMs * 4), kSortThreads, 0, s>>>(kin, m, passes, ws.ghist);
-    onesweep_scan<<<passes, 256, 0, s>>>(ws.ghist);
-    for (int p = 0; p < passes; ++p) {
-      ALTO_CUDA_TRY(cudaMemsetAsync(ws.counts, 0, static_cast<size_t>(otiles) * 256 * 4, s));
+    unsigned* ctr = ws.ghist + kMaxPasses * kOneBins;
+    ALTO_CUDA_TRY(cudaMemsetAsync(ws.ghist, 0, static_cast<size_t>(kMaxPasses) * (kOneBins + 1) * 4, s));
+    onesweep_hist<W><<<grid_for(m, kSortThreads, kSMs * 4), kSortThreads, 0, s>>>(kin, m, opasses, ws.ghist);
+    onesweep_scan<<<opasses, kOneBins, 0, s>>>(ws.ghist);
+    for (int p = 0; p < opasses; ++p) {
+      ALTO_CUDA_TRY(cudaMemsetAsync(ws.counts, 0, static_cast<size_t>(otiles) * kOneBins * 4, s));
       onesweep_pass<W, P, OT><<<static_cast<unsigned>(otiles), OT, osmem, s>>>(
-          kin, pin, kout, pout, m, 8 * p, ws.ghist + p * 256, ws.counts, ctr + p);
+          kin, pin, kout, pout, m, kOneBits * p, ws.ghist + p * kOneBins, ws.counts, ctr + p);
       std::swap(kin, kout);
       std::swap(pin, pout);
     }
