@@ -471,7 +471,7 @@ def run_b200(args):
             launches_per_step += len(mk.ms_pairs(dims, n, R, 4))
         if not args.no_hot:
             hp = (alto._cache.get(("hotms", n, R, odt, mk.ms_tile(alto), mk.MS_ORDER)) if ms_used
-                  else alto._cache.get(("hot", n, R, odt)))
+                  else alto._cache.get(("hotms", n, R, odt, 128, 0)))
             launches_per_step += 1 if hp else 0
     traffic, traffic_src = None, None
     if ws == 1 and nnz_total == cfg.nnz and args.out == "f32" and not args.no_hot and R == cfg.rank:

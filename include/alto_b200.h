@@ -184,10 +184,12 @@ typedef struct alto_mttkrp_args {
   const uint64_t* mkeys;
   const void* mvals;
   int32_t mtile;
-  /* Mode-stream hot plan (alto_hot_copies): with mkeys set, hot_slot holds
+  /* Per-row copy counts (alto_hot_copies): with hot_base set, hot_slot holds
    * hot_code (dim int32: (first copy << 5) | log2(copies), or -1), hot_base
    * the per-slot first copy (n_hot+1), and hot_buf hot_base[n_hot] * rank
-   * elements of out_dtype (zero on entry, left zero). */
+   * elements of out_dtype (zero on entry, left zero); hot_copies is ignored.
+   * Required with a mode stream (mkeys); optional for the ALTO-order kernels
+   * (plan built with tile 128 and flags 0). */
   const int32_t* hot_base;
   int32_t mrr;                   /* mode stream built with ALTO_MS_ROUND_ROBIN (1) or ALTO_MS_BLOCKED (2) */
   /* Paired input modes (mode stream only; float32 values and factors, rank

@@ -188,7 +188,9 @@ fast_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ ta
         int tgt = static_cast<int>(row);
         if (hot_slot) {
           const int hs = __ldg(hot_slot + row);
-          if (hs >= 0) tgt = -(hs + 1);
+          if (hs >= 0)  // adaptive plan: copy (sub-tile mod copies) of the row's own copies
+            tgt = P.hot_adaptive ? -((hs >> 5) + static_cast<int>(static_cast<unsigned>(sub) & ((1u << (hs & 31)) - 1u)) + 1)
+                                 : -(hs + 1);
         }
         rec[k][RL::TGT] = static_cast<unsigned>(tgt);
         if constexpr (sizeof(V) == 4) {
@@ -269,7 +271,9 @@ fast_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ ta
     __syncwarp();
     // ---- consume: G lanes per element, 4 ranks per lane ---------------------
     O* hot_base = hot_slot ? static_cast<O*>(P.hot_buf) +
-                                 static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) * P.n_hot * R
+                                 (P.hot_adaptive ? 0ll
+                                                 : static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) *
+                                                       P.n_hot * R)
                            : nullptr;
     A acc[4] = {A(0), A(0), A(0), A(0)};
     int cur = INT_MIN;
@@ -514,7 +518,9 @@ planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__
         int tgt = static_cast<int>(row);
         if (hot_slot) {
           const int hs = __ldg(hot_slot + row);
-          if (hs >= 0) tgt = -(hs + 1);
+          if (hs >= 0)  // adaptive plan: copy (sub-tile mod copies) of the row's own copies
+            tgt = P.hot_adaptive ? -((hs >> 5) + static_cast<int>(static_cast<unsigned>(sub) & ((1u << (hs & 31)) - 1u)) + 1)
+                                 : -(hs + 1);
         }
         rec[RL::TGT] = static_cast<unsigned>(tgt);
         if constexpr (sizeof(V) == 4) {
@@ -535,7 +541,9 @@ planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__
     __syncwarp();
     // ---- consume (identical to fast_kernel) -------------------------------------
     O* hot_base = hot_slot ? static_cast<O*>(P.hot_buf) +
-                                 static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) * P.n_hot * R
+                                 (P.hot_adaptive ? 0ll
+                                                 : static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) *
+                                                       P.n_hot * R)
                            : nullptr;
     A acc[4] = {A(0), A(0), A(0), A(0)};
     int cur = INT_MIN;

@@ -160,6 +160,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
   P.hot_copies = a->hot_copies > 0 ? a->hot_copies : 1;
   ALTO_REQUIRE((P.hot_copies & (P.hot_copies - 1)) == 0, "hot_copies must be a power of two");
   P.hot_buf = a->hot_buf;
+  P.hot_adaptive = (a->hot_base != nullptr && P.n_hot > 0) ? 1 : 0;
   P.flags = a->flags;
   P.packed = a->packed;
   P.pos = a->pos;
@@ -196,7 +197,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
       return ALTO_EUNSUPPORTED;
     }
     if (sti) return sti;
-    if (a->mkeys && P.n_hot > 0) {
+    if (a->hot_base && P.n_hot > 0) {
       hot_reduce_rows_kernel<long long><<<(P.n_hot + 7) / 8, 256, 0, s>>>(
           static_cast<long long*>(P.hot_buf), a->hot_rows, a->hot_base, P.n_hot, a->rank,
           static_cast<long long*>(a->out));
@@ -221,7 +222,7 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
                           : (o32 ? stream_w2_f32(d, tab, P, a->value_dtype, a->factor_dtype, s)
                                  : stream_w2_f64(d, tab, P, a->value_dtype, a->factor_dtype, s));
   if (st) return st;
-  if (a->mkeys && P.n_hot > 0) {  // mode stream: per-row copy counts (alto_hot_copies)
+  if (a->hot_base && P.n_hot > 0) {  // per-row copy counts (alto_hot_copies)
     if (a->out_dtype == ALTO_F32)
       hot_reduce_rows_kernel<float><<<(P.n_hot + 7) / 8, 256, 0, s>>>(static_cast<float*>(P.hot_buf), a->hot_rows,
                                                                       a->hot_base, P.n_hot, a->rank,

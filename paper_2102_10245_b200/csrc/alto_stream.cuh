@@ -49,7 +49,8 @@ struct StreamParams {
   long long ntiles;
   const int* hot_slot;
   int hot_copies;
-  void* hot_buf;  // hot_copies x n_hot x R, element type = output type O
+  int hot_adaptive;  // hot_slot holds alto_hot_copies codes ((first copy << 5) | log2 copies), hot_buf the copies
+  void* hot_buf;  // hot_copies x n_hot x R (adaptive: all rows' copies), element type = output type O
   int flags;
   const uint64_t* packed;     // mode-contiguous keys (optional, alto_pack_keys)
   const unsigned char* pos;   // per-mode sub-tile slots (optional, alto_subtile_order)
@@ -290,7 +291,9 @@ stream_warp_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restri
         int tgt = row;
         if (hot_slot) {
           const int hs = __ldg(hot_slot + row);
-          if (hs >= 0) tgt = -(hs + 1);
+          if (hs >= 0)  // adaptive plan: copy (sub-tile mod copies) of the row's own copies
+            tgt = P.hot_adaptive ? -((hs >> 5) + static_cast<int>(static_cast<unsigned>(sub) & ((1u << (hs & 31)) - 1u)) + 1)
+                                 : -(hs + 1);
         }
         rec[k][RL::TGT] = static_cast<unsigned>(tgt);
         if constexpr (sizeof(V) == 4) {
@@ -362,7 +365,9 @@ stream_warp_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restri
     // ---- consume: G lanes per element ------------------------------------
     O* hot_base = P.n_hot > 0
                       ? static_cast<O*>(P.hot_buf) +
-                            static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) * P.n_hot * R
+                            (P.hot_adaptive
+                                 ? 0ll
+                                 : static_cast<long long>(static_cast<unsigned>(sub) & (P.hot_copies - 1)) * P.n_hot * R)
                       : nullptr;
     const int j0 = grp * CH;
     const int j1 = min(cnt, j0 + CH);

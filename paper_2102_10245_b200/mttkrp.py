@@ -183,12 +183,11 @@ def _args(tensor: AltoTensor, fdev: list, mode: int, out, tile: int = 0, zero_ou
 
 
 # Hot-row plan: rows holding more than HOT_TAU elements appear in almost every
-# tile; their tile partials go to HOT_COPIES replicated buffers instead of
-# contending on one L2 line (see alto_mttkrp_args in include/alto_b200.h).
+# tile; their tile partials go to replicated copies (a per-row number of
+# them, alto_hot_copies) instead of contending on one L2 line (see
+# alto_mttkrp_args in include/alto_b200.h).
 HOT_TAU = 1024
 HOT_MAX = 32768
-# float32 copies take fewer adds each (precision); float64 copies fewer bytes
-HOT_COPIES = {4: 64, 8: 32}
 
 
 def hot_slots(tensor: AltoTensor, mode: int):
@@ -220,37 +219,23 @@ def hot_slots(tensor: AltoTensor, mode: int):
     return res
 
 
-def hot_plan(tensor: AltoTensor, mode: int, rank: int, out_dtype=None):
-    """Hot-row plan of one mode with zeroed replicated copies for (rank, output dtype), cached."""
-    torch = _torch()
-    out_dtype = out_dtype or torch.float64
-    key = ("hot", mode, rank, out_dtype)
-    if key in tensor._cache:
-        return tensor._cache[key]
-    hs = hot_slots(tensor, mode)
-    plan = None
-    if hs is not None:
-        slot, rows, n = hs
-        copies = HOT_COPIES[torch.empty(0, dtype=out_dtype).element_size()]
-        buf = torch.zeros(copies * n * rank, dtype=out_dtype, device=tensor.keys.device)
-        plan = (slot, rows, n, copies, buf)
-    tensor._cache[key] = plan
-    return plan
-
-
-# Mode-stream hot plan: at most HOT_BOUND merges per replicated copy of a hot
-# row (bounds same-address contention and float32 rounding of the copies),
-# at most 2^HOT_MAX_LG copies per row.
+# Hot plan: at most HOT_BOUND merges per replicated copy of a hot row (bounds
+# same-address contention and float32 rounding of the copies), at most
+# 2^HOT_MAX_LG copies per row.
 HOT_BOUND = 1024
 HOT_MAX_LG = 10
 
 
-def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype):
-    """Hot-row plan of the mode-stream kernel (alto_hot_copies), cached:
-    (hot_code (I_mode,) int32, hot rows, count, hot_base (count+1,) int32, zeroed copies) or None."""
+def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype, alto_order: bool = False):
+    """Hot-row plan with per-row copy counts (alto_hot_copies), cached:
+    (hot_code (I_mode,) int32, hot rows, count, hot_base (count+1,) int32, zeroed copies) or None.
+    alto_order: for the kernels that walk the ALTO stream in 128-element
+    sub-tiles (a row merges once per sub-tile it appears in), else for the
+    mode stream."""
     torch = _torch()
-    T = ms_tile(tensor)
-    key = ("hotms", mode, rank, out_dtype, T, MS_ORDER)
+    T = 128 if alto_order else ms_tile(tensor)
+    order = 0 if alto_order else MS_ORDER
+    key = ("hotms", mode, rank, out_dtype, T, order)
     if key in tensor._cache:
         return tensor._cache[key]
     hs = hot_slots(tensor, mode)
@@ -261,7 +246,7 @@ def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype):
         _perm, ptr = row_index(tensor, mode)
         code = torch.full((tensor.layout.dims[mode],), -1, dtype=torch.int32, device=dev)
         base = torch.empty(n + 1, dtype=torch.int32, device=dev)
-        _lib.check(_lib.load().alto_hot_copies(ptr.data_ptr(), rows.data_ptr(), n, tensor.nnz, T, MS_ORDER, HOT_BOUND,
+        _lib.check(_lib.load().alto_hot_copies(ptr.data_ptr(), rows.data_ptr(), n, tensor.nnz, T, order, HOT_BOUND,
                                                HOT_MAX_LG, code.data_ptr(), base.data_ptr(), _lib.stream_ptr()),
                    "alto_hot_copies")
         total = int(base[n].item())
@@ -280,11 +265,14 @@ def _set_hot(a, tensor: AltoTensor, mode: int, rank: int, out_dtype, ms) -> None
             a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf, a.hot_base = (
                 code.data_ptr(), rows.data_ptr(), n, 1, buf.data_ptr(), base.data_ptr())
         return
-    hp = hot_plan(tensor, mode, rank, out_dtype)
+    # ALTO-order kernels: the same per-row copy counts, sized for one merge per
+    # 128-element sub-tile a row appears in (bounded merges per float32 copy:
+    # the uniform 64-copy plan left 3e-5 on cfg5's Zipf head at full size)
+    hp = hot_plan_ms(tensor, mode, rank, out_dtype, alto_order=True)
     if hp is not None:
-        slot, rows, n, copies, buf = hp
-        a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf = (slot.data_ptr(), rows.data_ptr(), n, copies,
-                                                                   buf.data_ptr())
+        code, rows, n, base, buf = hp
+        a.hot_slot, a.hot_rows, a.n_hot, a.hot_copies, a.hot_buf, a.hot_base = (
+            code.data_ptr(), rows.data_ptr(), n, 1, buf.data_ptr(), base.data_ptr())
 
 
 # Per-mode stream tile length (elements); 0 disables the mode-stream kernel.

@@ -10,12 +10,11 @@ Per mode four device paths are checked:
                 pull, the Buffered scheme) with float32 factors and output:
                 <= 1e-5, and bitwise equal across two runs;
   * `alto`    - the single-copy ALTO-order kernel (packed keys + sub-tile
-                order, no per-mode stream), float32 output: <= 1e-5, except
-                cfg5 where its float32 merges of the Zipf-head rows (one per
-                128-element sub-tile, ~2-4M per head row, spread over 64
-                copies) measure 1.3-3.4e-5: bounded here at 5e-5 and
-                recorded as a reason the bench headline uses the mode
-                stream (DESIGN.md §4);
+                order, no per-mode stream), float32 output: <= 1e-5 (its
+                Zipf-head rows merge once per 128-element sub-tile, 2-4M
+                times per head row on cfg5: the per-row copy counts of
+                alto_hot_copies bound the float32 merges per copy; the
+                uniform 64-copy plan of round 1 measured 1.3-3.4e-5 there);
   * `api`     - the reference-facing default path `mttkrp(tensor, factors,
                 mode, partitions=16)` with float64 factors (auto plan =
                 Buffered on every mode, SURVEY §7.3 item 7 -> the
@@ -98,7 +97,7 @@ def test_fullsize_mttkrp_all_modes_vs_oracle(at, cfg, nnz):
     for mode, e in errs.items():
         assert e["stream"] <= tol_fast, (cfg, nnz, mode, e)
         if "alto" in e:
-            assert e["alto"] <= (5e-5 if cfg == 5 else tol_fast), (cfg, nnz, mode, e)
+            assert e["alto"] <= tol_fast, (cfg, nnz, mode, e)
         if "pull" in e:
             assert e["pull"] <= tol_fast, (cfg, nnz, mode, e)
         assert e["api"] <= (1e-10 if fp32 else 1e-12), (cfg, nnz, mode, e)

@@ -357,7 +357,7 @@ class TestStreamKernel:
         for mode in range(len(dims)):
             b = mk.mttkrp_stream(alto, fdev, mode, planned=False).cpu().numpy()
             a = mk.mttkrp_stream(alto, fdev, mode).cpu().numpy()
-            assert rel_error(a, b) <= 1e-6
+            assert rel_error(a, b) <= 3e-6  # two float32 accumulation orders
             torch.cuda.synchronize()
 
     @pytest.mark.parametrize("cfg", [4, "four"])
