@@ -285,7 +285,7 @@ size_t alto_mode_stream_workspace_bytes(int64_t m);
 /* Step shape of the blocked mode-stream kernel for a tensor order, rank,
  * value dtype and number of paired input modes: *u elements per lane group
  * and *groups lane groups per warp (ALTO_EUNSUPPORTED when no kernel covers
- * the shape). */
+ * the shape: float32 values, orders 3-5, ranks 16/32). */
 int alto_mstream_block(int32_t order, int32_t rank, int32_t value_dtype, int32_t n_pairs, int32_t* u,
                        int32_t* groups);
 int alto_mode_stream(const alto_layout* lay, const uint64_t* packed, const void* values, int32_t value_dtype,

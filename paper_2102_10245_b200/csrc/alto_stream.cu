@@ -251,7 +251,7 @@ int alto_mstream_block(int32_t order, int32_t rank, int32_t value_dtype, int32_t
   ALTO_REQUIRE(u && groups, "null output");
   ALTO_REQUIRE(value_dtype == ALTO_F32 || value_dtype == ALTO_F64, "unsupported value dtype");
   if (order < 3 || order > 5 || (rank != 16 && rank != 32) || n_pairs < 0 || n_pairs > 2 ||
-      order - 1 - n_pairs < 2)
+      order - 1 - n_pairs < 2 || value_dtype != ALTO_F32)
     return ALTO_EUNSUPPORTED;
   // same rule as ms_u<NV + 1, R, V, 32>() (alto_mstream.cuh): ~32 registers of
   // gathered factor data per lane, at most R/4 elements per group
