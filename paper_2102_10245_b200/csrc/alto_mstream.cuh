@@ -713,6 +713,8 @@ int mstream_dispatch(const DevLayout& d, MStream S, const StreamParams& P, cudaS
     }
     return ALTO_EUNSUPPORTED;
   }
+  // (round 2, same kernel with raw key words + value shuffled, 3 per element instead of 4 decoded words plus
+  // the increment scan, every lane decoding for itself: cfg2 0.476 vs 0.459, cfg5 6.4-7.0 vs 5.9-6.7 ms: dropped)
   // (measured and dropped on cfg2, ms/mode: broadcast key loads 0.70-0.72,
   // 4 CTAs/SM 0.64-0.68, a two-stage pipeline 0.65-0.88, a shared-memory
   // record exchange 0.66-0.68, raw-key shuffles 0.69-0.73 — against 0.45-0.46
