@@ -168,12 +168,8 @@ struct MStream {
 // L2P: factor rows are gathered with a per-table L2 range policy (the
 // table's first l2_hot bytes evict_last, the rest evict_first) and output
 // rows merged with evict_first (alto_mttkrp_args.l2_hot_bytes).
-// RAWX: the decoding lanes broadcast the raw key words and the value (3
-// shuffles per element for one-word keys) and every lane decodes them itself
-// (row increments summed locally), instead of broadcasting 4 decoded words
-// per element plus the increment scan.
 template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = 4, int NV = N - 1, bool DELTA = false,
-          bool L2P = false, bool RAWX = false>
+          bool L2P = false>
 __global__ void __launch_bounds__(kTileThreads, MINB)
 mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStream S,
                const __grid_constant__ StreamParams P) {
@@ -319,42 +315,6 @@ mstream_kernel(const __grid_constant__ DevLayout L, const __grid_constant__ MStr
           const Key<W> kk = nk;
           const V vv = nv;
           prefetch(j0 + U);
-          if constexpr (RAWX) {
-            static_assert(W == 1 && sizeof(V) == 4, "raw-key exchange: one-word keys, float32 values");
-            V4<F> g[U][NIN];
-            unsigned tg[U];
-            V vu[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              Key<W> ku;
-              const unsigned lo = __shfl_sync(0xffffffffu, static_cast<unsigned>(kk.w[0]), gbase + u);
-              const unsigned hi = __shfl_sync(0xffffffffu, static_cast<unsigned>(kk.w[0] >> 32), gbase + u);
-              ku.w[0] = (static_cast<uint64_t>(hi) << 32) | lo;
-              vu[u] = __shfl_sync(0xffffffffu, vv, gbase + u);
-              const bool ok = j0 + u < len;  // the group's own slice length: no exchange needed
-              unsigned row;
-              if constexpr (DELTA) {
-                carry += ok ? ms_field<W>(ku, fout) : 0u;
-                row = carry;
-              } else {
-                row = ms_field<W>(ku, fout);
-              }
-              tg[u] = ok ? (row | (hi & hotmask)) : 0xffffffffu;
-              if (ok) {
-#pragma unroll
-                for (int k = 0; k < NIN; ++k) {
-                  if constexpr (L2P)
-                    g[u][k] = gather_off_pol(fin_lane[k], voff(ku, k), gpol[k]);
-                  else
-                    g[u][k] = gather_off<F>(fin_lane[k], voff(ku, k));
-                }
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-              if (tg[u] != 0xffffffffu) consume(tg[u], vu[u], g[u]);
-            continue;
-          }
           unsigned moff[NIN];
 #pragma unroll
           for (int k = 0; k < NIN; ++k) moff[k] = voff(kk, k);
@@ -615,14 +575,9 @@ constexpr int ms_u() {
 }
 
 template <int W, typename V, typename O, int N, int R, int MINB = 3, int U = ms_u<N, R, V, 32>(), int NV = N - 1,
-          bool DELTA = false, bool L2P = false, bool RAWX = false>
+          bool DELTA = false, bool L2P = false>
 int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, cudaStream_t s) {
-  if constexpr (!L2P && !RAWX && W == 1 && N == 3 && R == 16 && NV == 2 && sizeof(V) == 4 &&
-                std::is_same<O, float>::value) {
-    if ((P.flags & 256) && S.rr == 1)  // experiment: raw-key exchange
-      return launch_mstream<W, V, O, N, R, MINB, U, NV, DELTA, false, true>(d, S, P, s);
-  }
-  if constexpr (!L2P && !RAWX && N == 3 && R == 16 && NV == 2 && sizeof(V) == 4 && std::is_same<O, float>::value) {
+  if constexpr (!L2P && N == 3 && R == 16 && NV == 2 && sizeof(V) == 4 && std::is_same<O, float>::value) {
     // L2 residency policies requested for an input factor (order 3, rank 16, float32)
     bool want = false;
     for (int n = 0; n < 3; ++n) want = want || (n != P.mode && P.l2_hot[n] > 0);
@@ -670,7 +625,7 @@ int launch_mstream(const DevLayout& d, const MStream& S, const StreamParams& P, 
     return ALTO_OK;
     }
   }
-  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, NV, DELTA, L2P, RAWX>;
+  auto kern = mstream_kernel<W, V, O, N, R, MINB, U, NV, DELTA, L2P>;
   static int cached_bps = 0;
   if (!cached_bps) {
     int b = 1;
