@@ -209,9 +209,14 @@ class TestStreamKernel:
                 assert rel_error(out, ref) <= tol, (cfg, mode, tile, rel_error(out, ref))
             torch.cuda.synchronize()
 
-    @pytest.mark.parametrize("cfg,nnz,rank", [(2, 400_000, 16), (3, 150_000, 32), (4, 300_000, 16)])
+    @pytest.mark.parametrize("cfg,nnz,rank", [(2, 400_000, 16), (3, 150_000, 32), (4, 300_000, 16),
+                                              (3, 150_000, 16), (5, 200_000, 32), (4, 200_000, 32)])
     def test_float32_output(self, at, cfg, nnz, rank):
-        """float32 output (RED.F32x4 merge, hot rows in float64) vs the fp64 oracle at 1e-5."""
+        """float32 output (RED.F32x4 merge, hot rows in float64) vs the fp64 oracle at 1e-5.
+        The (cfg, rank) pairs cover the cooperative kernel (order 3, rank 16), the blocked
+        kernel at rank 32 (orders 3-5, one-word delta keys on the 128-bit layouts of cfg3 /
+        cfg5, two-word keys on cfg3's short modes) and with paired input modes (cfg4 and
+        cfg3 at rank 16: pairs + delta keys)."""
         import torch
 
         from paper_2102_10245_b200.mttkrp import factors_to_device, mttkrp_stream
