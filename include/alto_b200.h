@@ -391,6 +391,13 @@ typedef struct alto_pull_args {
   double* part;                 /* (n_chunks, rank) float64 chunk partials   */
   const int32_t* slice_rows;    /* (nslices, 2) first / last row per slice (alto_pull_slice_rows) */
   const int32_t* mbase;         /* delta stream (ALTO_MS_DELTA): each slice's first row, else NULL */
+  /* Paired input modes, as in alto_mttkrp_args (float32 values and factors,
+   * rank 16, orders 4-5): pair_tab[i] = alto_krp_pair table of modes
+   * pair_a[i], pair_b[i]; one gather replaces two. */
+  int32_t n_pairs;
+  int32_t pair_a[2];
+  int32_t pair_b[2];
+  const void* pair_tab[2];
 } alto_pull_args;
 int alto_mttkrp_pull(const alto_pull_args* a, void* stream);
 /* Plan helper: first and last output row of every slice of a mode stream,

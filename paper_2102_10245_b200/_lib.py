@@ -102,6 +102,10 @@ class CPullArgs(Structure):
         ("part", c_void_p),
         ("slice_rows", c_void_p),
         ("mbase", c_void_p),
+        ("n_pairs", c_int32),
+        ("pair_a", c_int32 * 2),
+        ("pair_b", c_int32 * 2),
+        ("pair_tab", c_void_p * 2),
     ]
 
 

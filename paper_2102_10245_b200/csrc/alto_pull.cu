@@ -43,6 +43,26 @@ int alto_mttkrp_pull(const alto_pull_args* a, void* stream) {
   S.dim = dim;
   S.f = f;
   for (int n = 0; n < ALTO_MAX_ORDER; ++n) S.factors[n] = n < d.order ? a->factors[n] : nullptr;
+  ALTO_REQUIRE(a->n_pairs >= 0 && a->n_pairs <= 2, "at most 2 paired input modes");
+  if (a->n_pairs > 0) {
+    // gathered inputs: the pairs' product tables, then the unpaired input factors (alto_krp_pair; same
+    // rules as alto_mttkrp_args.pair_*)
+    ALTO_REQUIRE(a->factor_dtype == ALTO_F32 && a->value_dtype == ALTO_F32 && a->rank == 16 && d.order >= 4,
+                 "paired input modes need float32 data, rank 16 and order 4 or 5");
+    int nv = 0;
+    unsigned used = 1u << a->mode;
+    for (int i = 0; i < a->n_pairs; ++i) {
+      const int pa = a->pair_a[i], pb = a->pair_b[i];
+      ALTO_REQUIRE(pa >= 0 && pb >= 0 && pa < d.order && pb < d.order && pa != pb && !((used >> pa) & 1u) &&
+                       !((used >> pb) & 1u) && a->pair_tab[i] &&
+                       d.dims[pa] * d.dims[pb] * a->rank * 4ll <= 0xFFFFFFFFll,
+                   "bad input-mode pair");
+      used |= (1u << pa) | (1u << pb);
+      S.vin[nv++] = VIn{a->pair_tab[i], pa, pb, static_cast<unsigned>(d.dims[pb])};
+    }
+    for (int n = 0; n < d.order; ++n)
+      if (!((used >> n) & 1u)) S.vin[nv++] = VIn{a->factors[n], n, -1, 1u};
+  }
   S.out = a->out;
   S.rec = a->rec;
   S.slice_rec = reinterpret_cast<const int2*>(a->slice_rec);

@@ -56,6 +56,7 @@ struct PullStage {
   void* rec;              // (n_rec, R) A: shared-row partials (Buffered)
   const int2* slice_rec;  // (nslices) record slot of the slice's first / last run, -1 if owned
   const int2* slice_rows; // (nslices) first / last output row of every slice (alto_pull_slice_rows)
+  VIn vin[ALTO_MAX_ORDER]; // gathered inputs when input modes are paired (alto_krp_pair tables), as in MStream
 };
 
 template <typename O, typename A>
@@ -95,13 +96,17 @@ __device__ __forceinline__ void red_row4(O* p, const A (&a)[4]) {
 // DELTA: one-word delta stream keys (ALTO_MS_DELTA): the output field holds the
 // row increment from the previous element of the slice; the slice's first row
 // comes from slice_rows.
-template <int W, typename V, typename F, typename O, int N, int R, int U, bool ATOMIC, bool DELTA = false>
+// NV < N - 1: paired input modes — one gather from a row-wise product table
+// replaces two (S.vin, float32 factors, rank 16, orders 4-5).
+template <int W, typename V, typename F, typename O, int N, int R, int U, bool ATOMIC, bool DELTA = false,
+          int NV = N - 1>
 __global__ void __launch_bounds__(256, (sizeof(F) == 4 ? 3 : 2))
 pull_stage_kernel(const __grid_constant__ PullStage S) {
   using A = F;
   constexpr int G = R / 4;     // lanes per slice
   constexpr int GPW = 32 / G;  // slices per warp
-  constexpr int NIN = N - 1;
+  constexpr int NIN = NV;
+  constexpr bool PAIR = NV < N - 1;
   constexpr unsigned ROWB = static_cast<unsigned>(R * sizeof(F));
   static_assert(R % 4 == 0 && G >= 1 && G <= 32 && 32 % G == 0, "rank must be 4 * a power of two <= 128");
   static_assert(U >= 1 && U <= G, "one decoding lane per element of a block");
@@ -112,11 +117,21 @@ pull_stage_kernel(const __grid_constant__ PullStage S) {
   const int gbase = lane & ~(G - 1);
   const char* fin_lane[NIN];
   FSel fin[NIN];
+  FSel finb[PAIR ? NIN : 1];
+  unsigned vdb[PAIR ? NIN : 1];
 #pragma unroll
   for (int k = 0; k < NIN; ++k) {
-    const int n = k < S.mode ? k : k + 1;
-    fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(S.factors[n]) + 4 * gl);
-    fin[k] = fsel_of(S.f, n);
+    if constexpr (PAIR) {
+      const VIn& vi = S.vin[k];
+      fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(vi.tab) + 4 * gl);
+      fin[k] = fsel_of(S.f, vi.na);
+      finb[k] = vi.nb >= 0 ? fsel_of(S.f, vi.nb) : FSel{0u, 0u, false};  // empty field reads 0
+      vdb[k] = vi.nb >= 0 ? vi.db : 1u;
+    } else {
+      const int n = k < S.mode ? k : k + 1;
+      fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(S.factors[n]) + 4 * gl);
+      fin[k] = fsel_of(S.f, n);
+    }
   }
   const FSel fout = fsel_of(S.f, S.mode);
   const V* __restrict__ vals = static_cast<const V*>(S.vals);
@@ -201,7 +216,12 @@ pull_stage_kernel(const __grid_constant__ PullStage S) {
       prefetch(j0 + U);
       unsigned mrow[NIN];
 #pragma unroll
-      for (int k = 0; k < NIN; ++k) mrow[k] = ms_field<W>(kk, fin[k]);
+      for (int k = 0; k < NIN; ++k) {
+        if constexpr (PAIR)
+          mrow[k] = ms_field<W>(kk, fin[k]) * vdb[k] + ms_field<W>(kk, finb[k]);
+        else
+          mrow[k] = ms_field<W>(kk, fin[k]);
+      }
       int mtg;
       if constexpr (DELTA) {
         // rows = carry + inclusive prefix of the U decoded increments

@@ -14,11 +14,11 @@ constexpr int pull_u() {
   return std::min(R / 4, ub);
 }
 
-template <int W, typename V, typename F, typename O, int N, int R, bool AT, bool DELTA = false>
+template <int W, typename V, typename F, typename O, int N, int R, bool AT, bool DELTA = false, int NV = N - 1>
 int pull_launch(const alto_pull_args* a, const PullStage& S, cudaStream_t s) {
   using A = F;
-  constexpr int U = pull_u<N, R, F>();
-  auto kern = pull_stage_kernel<W, V, F, O, N, R, U, AT, DELTA>;
+  constexpr int U = pull_u<NV + 1, R, F>();
+  auto kern = pull_stage_kernel<W, V, F, O, N, R, U, AT, DELTA, NV>;
   static int bps = 0;
   if (!bps) {
     int b = 1;
@@ -53,6 +53,16 @@ int pull_launch(const alto_pull_args* a, const PullStage& S, cudaStream_t s) {
 template <int W, typename V, typename F, typename O, bool AT, bool DELTA = false>
 int pull_by_shape(const alto_pull_args* a, const PullStage& S, int order, cudaStream_t s) {
   const int R = a->rank;
+  if (a->n_pairs > 0) {
+    // paired input modes: float32 factors, rank 16, orders 4-5 (as the mode-stream kernel)
+    if constexpr (sizeof(F) == 4 && sizeof(V) == 4) {
+      if (R != 16) return ALTO_EUNSUPPORTED;
+      if (order == 4 && a->n_pairs == 1) return pull_launch<W, V, F, O, 4, 16, AT, DELTA, 2>(a, S, s);
+      if (order == 5 && a->n_pairs == 1) return pull_launch<W, V, F, O, 5, 16, AT, DELTA, 3>(a, S, s);
+      if (order == 5 && a->n_pairs == 2) return pull_launch<W, V, F, O, 5, 16, AT, DELTA, 2>(a, S, s);
+    }
+    return ALTO_EUNSUPPORTED;
+  }
 #define ALTO_PULL_N(NN)                                                                  \
   if (order == NN) {                                                                     \
     if (R == 16) return pull_launch<W, V, F, O, NN, 16, AT, DELTA>(a, S, s);             \

@@ -745,6 +745,9 @@ def mttkrp_pull(tensor: AltoTensor, fdev: list, mode: int, out=None, out_dtype=N
     a.slice_rec = plan["slice_rec"].data_ptr()
     a.slice_rows = plan["slice_rows"].data_ptr()
     a.mbase = None if ps[3] is None else ps[3].data_ptr()
+    tabs = []  # product tables of paired input modes: stream-ordered, released after the launch
+    if fb == 4 and vals.dtype == torch.float32:
+        _set_pairs(a, tensor, fdev, mode, tabs)
     rec = part = None
     if not atomic and plan["n_rec"]:
         rec = torch.empty((plan["n_rec"], rank), dtype=fdev[0].dtype, device=out.device)
