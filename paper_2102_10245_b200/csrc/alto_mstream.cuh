@@ -723,6 +723,21 @@ __global__ void __launch_bounds__(256) hot_reduce_rows_kernel(O* __restrict__ bu
   const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (slot >= n_hot) return;
   const int lane = threadIdx.x & 31;
+  if (R > 32 || (R & (R - 1)) != 0) {
+    // generic kernel's ranks (above 32, or not a power of two): lane r, r+32, ... sums its rank over the
+    // copies in order
+    for (int r = lane; r < R; r += 32) {
+      S acc = S(0);
+      for (int k = hot_base[slot]; k < hot_base[slot + 1]; ++k) {
+        O* p = buf + static_cast<long long>(k) * R + r;
+        acc += static_cast<S>(*p);
+        *p = O(0);
+      }
+      O* o = out + static_cast<long long>(hot_rows[slot]) * R + r;
+      *o = static_cast<O>(static_cast<S>(*o) + acc);
+    }
+    return;
+  }
   const int per = R >= 32 ? 1 : 32 / R;
   const int r = lane % R, j = lane / R;
   const bool active = R >= 32 ? (lane < R) : (j < per);
