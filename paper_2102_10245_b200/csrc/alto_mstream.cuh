@@ -429,7 +429,9 @@ __device__ __forceinline__ unsigned ms_sel(const Key<W>& k, const MsSel& f) {
 // register writeback, so the load/store pipe total does not drop there while
 // the redundant decode adds instructions) — the host picks per shape.  A
 // variant staging the stream through shared memory with cp.async (no
-// prefetch registers) was slower everywhere (cfg2 0.53, cfg3 3.0-3.4 ms).
+// prefetch registers) was slower everywhere (cfg2 0.53, cfg3 3.0-3.4 ms), and
+// 2 instead of 4 elements per group for the paired order-5 shape (62-72
+// registers, no spill, also at 4 CTAs/SM) ran cfg4 at 0.259-0.280 vs 0.240.
 template <int W, typename V, typename O, int N, int R, int MINB, int U, int NV, bool DELTA>
 __global__ void __launch_bounds__(kTileThreads, MINB)
 mstream_blk_kernel(const __grid_constant__ MStream S, const __grid_constant__ MsBlk Q,
