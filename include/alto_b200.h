@@ -192,7 +192,7 @@ typedef struct alto_mttkrp_args {
    * (plan built with tile 128 and flags 0). */
   const int32_t* hot_base;
   int32_t mrr;                   /* mode stream built with ALTO_MS_ROUND_ROBIN (1) or ALTO_MS_BLOCKED (2) */
-  /* Paired input modes (mode stream only; float32 values and factors, rank
+  /* Paired input modes (mode stream, or packed + pos; float32 values and factors, rank
    * 16, orders 4-5): input modes pair_a[i], pair_b[i] (i < n_pairs, disjoint,
    * not `mode`) are gathered together as one row of pair_tab[i], the
    * row-wise product table of their factors (alto_krp_pair: row

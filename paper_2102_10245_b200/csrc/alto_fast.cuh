@@ -432,17 +432,28 @@ __device__ __forceinline__ unsigned packed_field32(const Key<W>& k, int off, int
   return fast_field<W>(w, off, nb);
 }
 
-template <int W, typename V, typename O, int N, int R, int MINB = 3, int UF = 2>
+// Gathered inputs of the planned kernel when input modes are paired (float32,
+// rank 16, orders 4-5; alto_krp_pair tables): input k is the table `tab` with
+// row c[na] * db + c[nb] (nb < 0: a plain factor, row c[na]).
+struct PlanIn {
+  const void* tab[ALTO_MAX_ORDER];
+  int na[ALTO_MAX_ORDER], nb[ALTO_MAX_ORDER];
+  unsigned db[ALTO_MAX_ORDER];
+};
+
+template <int W, typename V, typename O, int N, int R, int MINB = 3, int UF = 2, int NV = N - 1>
 __global__ void __launch_bounds__(kTileThreads, MINB)
 planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ packed,
-               const unsigned char* __restrict__ pos, const __grid_constant__ StreamParams P) {
+               const unsigned char* __restrict__ pos, const __grid_constant__ StreamParams P,
+               const __grid_constant__ PlanIn Q) {
   using F = V;
   using A = V;
   constexpr int G = R / 4;
   constexpr int GPW = 32 / G;
   constexpr int CH = kFastTile / GPW;
-  constexpr int NIN = N - 1;
-  using RL = RecLayout<N, V>;
+  constexpr int NIN = NV;
+  constexpr bool PAIR = NV < N - 1;
+  using RL = RecLayout<NV + 1, V>;
   constexpr int NW = RL::NW;
   constexpr int EPL = kFastTile / 32;
   constexpr int U = UF;
@@ -457,8 +468,12 @@ planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__
   const char* fin_lane[NIN];
 #pragma unroll
   for (int k = 0; k < NIN; ++k) {
-    const int n = k < mode ? k : k + 1;
-    fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(P.factors[n]) + 4 * gl);
+    if constexpr (PAIR) {
+      fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(Q.tab[k]) + 4 * gl);
+    } else {
+      const int n = k < mode ? k : k + 1;
+      fin_lane[k] = reinterpret_cast<const char*>(static_cast<const F*>(P.factors[n]) + 4 * gl);
+    }
   }
   int pack_off[N], bits[N];
 #pragma unroll
@@ -514,7 +529,16 @@ planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__
           if (n == mode) row = c[n];
         unsigned rec[NW];
 #pragma unroll
-        for (int q = 0; q < NIN; ++q) rec[q] = ((q < mode) ? c[q] : c[q + 1]) * ROWB;
+        for (int q = 0; q < NIN; ++q) {
+          if constexpr (PAIR) {
+            // decoded again with the pair's run-time modes (indexing c[] by them would spill it)
+            const unsigned ca = packed_field32<W>(kk[k], L.pack_off[Q.na[q]], L.bits[Q.na[q]]);
+            const unsigned cb = Q.nb[q] >= 0 ? packed_field32<W>(kk[k], L.pack_off[Q.nb[q]], L.bits[Q.nb[q]]) : 0u;
+            rec[q] = (ca * Q.db[q] + cb) * ROWB;
+          } else {
+            rec[q] = ((q < mode) ? c[q] : c[q + 1]) * ROWB;
+          }
+        }
         int tgt = static_cast<int>(row);
         if (hot_slot) {
           const int hs = __ldg(hot_slot + row);
@@ -617,13 +641,13 @@ planned_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__
   }
 }
 
-template <int W, typename V, typename O, int N, int R>
+template <int W, typename V, typename O, int N, int R, int NV = N - 1>
 int launch_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packed, const unsigned char* pos,
-                   cudaStream_t s) {
-  constexpr int NW = RecLayout<N, V>::NW;
+                   cudaStream_t s, const PlanIn& Q = PlanIn{}) {
+  constexpr int NW = RecLayout<NV + 1, V>::NW;
   constexpr int GPW = 32 / (R / 4);
   const size_t smem = (kTileThreads / 32) * (static_cast<size_t>(kFastTile) * NW + GPW * 4) * 4;
-  auto kern = planned_kernel<W, V, O, N, R>;
+  auto kern = planned_kernel<W, V, O, N, R, 3, 2, NV>;
   static size_t cached_smem = 0;
   static int cached_bps = 0;
   if (cached_smem != smem) {
@@ -636,7 +660,7 @@ int launch_planned(const DevLayout& d, const StreamParams& P, const uint64_t* pa
   const long long nsub = (P.m + kFastTile - 1) / kFastTile;
   const long long need = (nsub + kTileThreads / 32 - 1) / (kTileThreads / 32);
   const long long grid = std::min<long long>(need, static_cast<long long>(device_sms()) * std::max(cached_bps, 1));
-  kern<<<static_cast<unsigned>(grid), kTileThreads, smem, s>>>(d, packed, pos, P);
+  kern<<<static_cast<unsigned>(grid), kTileThreads, smem, s>>>(d, packed, pos, P, Q);
   ALTO_LAUNCH_CHECK("alto_mttkrp(planned)");
   return ALTO_OK;
 }
@@ -650,6 +674,39 @@ int try_planned(const DevLayout& d, const StreamParams& P, const uint64_t* packe
   if (maxdim * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll) return ALTO_EUNSUPPORTED;
   for (int n = 0; n < d.order; ++n)
     if (d.bits[n] > 31) return ALTO_EUNSUPPORTED;
+  if (P.n_pairs > 0) {
+    // paired input modes (alto_krp_pair tables): float32 data, rank 16, orders 4-5
+    if constexpr (sizeof(V) == 4 && !std::is_same<O, long long>::value) {
+      if (P.rank != 16 || d.order < 4) return ALTO_EUNSUPPORTED;
+      PlanIn Q{};
+      int nv = 0;
+      unsigned used = 1u << P.mode;
+      for (int i = 0; i < P.n_pairs; ++i) {
+        const int a = P.pair_a[i], b = P.pair_b[i];
+        if (a < 0 || b < 0 || a >= d.order || b >= d.order || a == b || ((used >> a) & 1u) || ((used >> b) & 1u) ||
+            !P.pair_tab[i] || d.dims[a] * d.dims[b] * P.rank * static_cast<long long>(sizeof(V)) > 0xFFFFFFFFll)
+          return ALTO_EUNSUPPORTED;
+        used |= (1u << a) | (1u << b);
+        Q.tab[nv] = P.pair_tab[i];
+        Q.na[nv] = a;
+        Q.nb[nv] = b;
+        Q.db[nv] = static_cast<unsigned>(d.dims[b]);
+        ++nv;
+      }
+      for (int n = 0; n < d.order; ++n)
+        if (!((used >> n) & 1u)) {
+          Q.tab[nv] = P.factors[n];
+          Q.na[nv] = n;
+          Q.nb[nv] = -1;
+          Q.db[nv] = 1u;
+          ++nv;
+        }
+      if (d.order == 4 && nv == 2) return launch_planned<W, V, O, 4, 16, 2>(d, P, packed, pos, s, Q);
+      if (d.order == 5 && nv == 3) return launch_planned<W, V, O, 5, 16, 3>(d, P, packed, pos, s, Q);
+      if (d.order == 5 && nv == 2) return launch_planned<W, V, O, 5, 16, 2>(d, P, packed, pos, s, Q);
+    }
+    return ALTO_EUNSUPPORTED;
+  }
   if (P.rank == 16) {
     if (d.order == 3) return launch_planned<W, V, O, 3, 16>(d, P, packed, pos, s);
     if (d.order == 4) return launch_planned<W, V, O, 4, 16>(d, P, packed, pos, s);

@@ -176,7 +176,8 @@ int alto_mttkrp(const alto_mttkrp_args* a, void* stream) {
     P.l2_tab[n] = static_cast<unsigned>(std::min<unsigned long long>(tb, 0xFFFFFFFFull));
     P.l2_hot[n] = on ? std::min(a->l2_hot_bytes[n], P.l2_tab[n]) : 0u;
   }
-  P.n_pairs = (a->mkeys && a->out_dtype != ALTO_I64) ? std::max(0, std::min(a->n_pairs, 2)) : 0;
+  P.n_pairs = ((a->mkeys || (a->packed && a->pos)) && a->out_dtype != ALTO_I64) ? std::max(0, std::min(a->n_pairs, 2))
+                                                                                 : 0;
   ALTO_REQUIRE(a->n_pairs <= 2, "at most 2 paired input modes");
   for (int i = 0; i < 2; ++i) {
     P.pair_a[i] = a->pair_a[i];

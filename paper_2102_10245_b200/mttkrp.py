@@ -554,6 +554,9 @@ def mttkrp_stream(tensor: AltoTensor, fdev: list, mode: int, out=None, tile: int
         # the single ALTO-order copy: packed keys + per-mode sub-tile order
         a.packed = packed_keys(tensor).data_ptr()
         a.pos = subtile_order(tensor, mode).data_ptr()
+        tabs = []  # product tables of paired input modes (orders 4-5, rank 16, float32)
+        if out.dtype != torch.int64:
+            _set_pairs(a, tensor, fdev, mode, tabs)
     if hot:
         _set_hot(a, tensor, mode, rank, out.dtype, ms)
     _lib.check(_lib.load().alto_mttkrp(ctypes.byref(a), _lib.stream_ptr()), "alto_mttkrp")

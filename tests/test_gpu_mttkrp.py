@@ -394,6 +394,9 @@ class TestStreamKernel:
             monkeypatch.setattr(mk, "MS_PAIR_BYTES", 64 << 20)
             assert rel_error(a, ref) <= 1e-5
             assert rel_error(a, b) <= 1e-6
+            # the ALTO-order single-copy kernel gathers the same product tables
+            p = mk.mttkrp_stream(alto, fdev, mode, planned="pos").cpu().numpy()
+            assert rel_error(p, ref) <= 1e-5
         pa, pb = mk.ms_pairs(dims, 0, 16, 4)[0]
         tab = torch.empty((dims[pa] * dims[pb], 16), dtype=torch.float32, device="cuda")
         from paper_2102_10245_b200 import _lib
