@@ -317,6 +317,8 @@ def run_b200(args):
     from paper_2102_10245_b200.layout import build_masks
 
     mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+    if getattr(args, "l2_hot_mb", None) is not None:
+        mk.MS_L2_HOT_MB = args.l2_hot_mb
     ws, rank, local = dist_env()
     # functional check of the multi-rank path on a one-GPU box only
     # (ALTO_BENCH_TEST_GLOO=1: every rank on cuda:0, gloo collectives; numbers
@@ -683,6 +685,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-cpals", action="store_true")
     ap.add_argument("--no-hot", action="store_true", help="disable the hot-row plan (A/B)")
+    ap.add_argument("--l2-hot-mb", type=float, default=None,
+                    help="L2 residency budget (MB) for the gathered factors (mttkrp.MS_L2_HOT_MB; A/B)")
     ap.add_argument("--out", default=None, choices=["f32", "f64"],
                     help="MTTKRP output dtype of the bench step (default: the config's value dtype)")
     ap.add_argument("--gen", default="device", choices=["device", "host"],
