@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
 
@@ -395,3 +396,16 @@ def cpd_als(tensor: AltoTensor, rank: int, max_iters: int = 50, tol: float = 1e-
     model = CpModel(factors=[f.cpu().numpy() for f in st.f64], weights=st.lam.cpu().numpy(),
                     fit_history=history, iterations=iters)
     return model
+
+
+def save_factors_csv(model: "CpModel", out_dir: str, prefix: str = "factor") -> list:
+    """One CSV per factor matrix, `<prefix>_<mode>.csv` with one-based mode
+    numbers, a row per index (cpd.py:231-242); returns the paths written.
+    Host I/O, not on the device path."""
+    os.makedirs(out_dir, exist_ok=True)
+    paths = []
+    for n, fac in enumerate(model.factors, start=1):
+        path = os.path.join(out_dir, f"{prefix}_{n}.csv")
+        np.savetxt(path, np.asarray(fac), delimiter=",")
+        paths.append(path)
+    return paths

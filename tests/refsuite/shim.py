@@ -6,7 +6,7 @@ the device path.  The shim package is written into a scratch directory:
   altotensor/layout.py, format.py, mttkrp.py, cpd.py
       re-export paper_2102_10245_b200's modules (the B200 hot path), plus
       the reference's out-of-scope reporting names (storage_stats /
-      StorageStats, save_factors_csv) taken from the unmodified reference;
+      StorageStats) taken from the unmodified reference;
   altotensor/__init__.py, coo.py, container.py, cli.py
       copied verbatim from the installed reference (baseline/_ref): the
       modules SURVEY §2 keeps out of scope; their relative imports
@@ -28,7 +28,7 @@ HOT = {
     "layout": ("from _altoref.layout import StorageStats, storage_stats  # reporting (out of scope)\n"),
     "format": "",
     "mttkrp": "",
-    "cpd": ("from _altoref.cpd import save_factors_csv  # CSV export (out of scope)\n"),
+    "cpd": "",
 }
 
 
