@@ -425,7 +425,7 @@ def run_b200(args):
                 mk.mttkrp_stream(small, fdev, n, out=outs[n], planned="pos")
     del small
     torch.cuda.synchronize()
-    ms_keys = ("mstream", "hotms", "hotslots", "row_index", "packed")
+    ms_keys = ("mstream", "hotms", "hotslots", "row_index", "row_ptr", "packed")
     plans = {"mode_stream": plan_leg(build_ms_plans, ms_keys)}
 
     def step_stream(n):

@@ -416,7 +416,7 @@ int alto_pull_slice_rows(const alto_layout* lay, const uint64_t* mkeys, int64_t 
 size_t alto_row_index_workspace_bytes(int64_t m, int64_t dim);
 int alto_row_index(const alto_layout* lay, const void* d_tables,
                    const uint64_t* keys, int64_t m, int32_t mode,
-                   int32_t* row_perm /* (M,) */, int64_t* row_ptr /* (dim+1,) */,
+                   int32_t* row_perm /* (M,), or NULL: row_ptr only */, int64_t* row_ptr /* (dim+1,) */,
                    void* workspace, size_t workspace_bytes, void* stream);
 int alto_mttkrp_exact(const alto_mttkrp_args* a, const int32_t* row_perm,
                       const int64_t* row_ptr, const int64_t* part_off,

@@ -225,9 +225,14 @@ int alto_row_index(const alto_layout* lay, const void* d_tables, const uint64_t*
   void* sort_ws = static_cast<char*>(workspace) + a;
   int st = alto_delinearize(lay, d_tables, keys, m, mode, reinterpret_cast<int64_t*>(rows), stream);
   if (st) return st;
-  iota_u32<<<grid_for(m, 256), 256, 0, s>>>(reinterpret_cast<unsigned*>(row_perm), m);
-  ALTO_LAUNCH_CHECK("alto_row_index/iota");
-  st = alto_sort_pairs(rows, row_perm, m, 1, 4, lay->bits[mode], sort_ws, workspace_bytes - a, stream);
+  if (row_perm) {
+    iota_u32<<<grid_for(m, 256), 256, 0, s>>>(reinterpret_cast<unsigned*>(row_perm), m);
+    ALTO_LAUNCH_CHECK("alto_row_index/iota");
+    st = alto_sort_pairs(rows, row_perm, m, 1, 4, lay->bits[mode], sort_ws, workspace_bytes - a, stream);
+  } else {
+    // row_ptr only (hot-row plans need the rows' element counts, not the permutation): keys-only sort
+    st = alto_sort_pairs(rows, nullptr, m, 1, 0, lay->bits[mode], sort_ws, workspace_bytes - a, stream);
+  }
   if (st) return st;
   row_ptr_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(rows, m, dim, reinterpret_cast<long long*>(row_ptr));
   ALTO_LAUNCH_CHECK("alto_row_index/row_ptr");

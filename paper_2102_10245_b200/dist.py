@@ -235,9 +235,9 @@ class DeviceOps:
         self.lib = _lib.load()
 
     def touched_rows(self, mode: int):
-        from .mttkrp import row_index
+        from .mttkrp import row_ptr
 
-        _perm, ptr = row_index(self.shard, mode)
+        ptr = row_ptr(self.shard, mode)
         return (ptr[1:] - ptr[:-1]) > 0
 
     def mttkrp(self, factors, mode: int):

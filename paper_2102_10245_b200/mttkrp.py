@@ -202,7 +202,7 @@ def hot_slots(tensor: AltoTensor, mode: int):
         lib = _lib.load()
         dim = tensor.layout.dims[mode]
         dev = tensor.keys.device
-        _perm, ptr = row_index(tensor, mode)
+        ptr = row_ptr(tensor, mode)
         slot = torch.empty(dim, dtype=torch.int32, device=dev)
         kk = min(HOT_MAX, dim)
         rows = torch.empty(kk, dtype=torch.int32, device=dev)
@@ -243,7 +243,7 @@ def hot_plan_ms(tensor: AltoTensor, mode: int, rank: int, out_dtype, alto_order:
     if hs is not None:
         _slot, rows, n = hs
         dev = tensor.keys.device
-        _perm, ptr = row_index(tensor, mode)
+        ptr = row_ptr(tensor, mode)
         code = torch.full((tensor.layout.dims[mode],), -1, dtype=torch.int32, device=dev)
         base = torch.empty(n + 1, dtype=torch.int32, device=dev)
         _lib.check(_lib.load().alto_hot_copies(ptr.data_ptr(), rows.data_ptr(), n, tensor.nnz, T, order, HOT_BOUND,
@@ -769,6 +769,32 @@ def mttkrp_pull(tensor: AltoTensor, fdev: list, mode: int, out=None, out_dtype=N
     return out
 
 
+def row_ptr(tensor: AltoTensor, mode: int):
+    """Per-mode row offsets (I_mode + 1,) int64 — the rows' element counts, which is all the
+    hot-row plans need: the row index's if it is cached, else alto_row_index without the
+    permutation (keys-only sort, no 4-byte-per-element array kept)."""
+    torch = _torch()
+    hit = tensor._cache.get(("row_index", mode))
+    if hit is not None:
+        return hit[1]
+    key = ("row_ptr", mode)
+    ptr = tensor._cache.get(key)
+    if ptr is None:
+        lib = _lib.load()
+        lay = tensor.layout
+        m = tensor.nnz
+        dim = lay.dims[mode]
+        dev = tensor.keys.device
+        ptr = torch.empty(dim + 1, dtype=torch.int64, device=dev)
+        ws_bytes = lib.alto_row_index_workspace_bytes(m, dim)
+        ws = torch.empty(max(int(ws_bytes), 8), dtype=torch.uint8, device=dev)
+        _lib.check(lib.alto_row_index(c_layout(lay), device_tables(lay).data_ptr(), tensor.keys.data_ptr(), m, mode,
+                                      None, ptr.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr()),
+                   "alto_row_index(row_ptr)")
+        tensor._cache[key] = ptr
+    return ptr
+
+
 def row_index(tensor: AltoTensor, mode: int):
     """Per-mode (row_perm, row_ptr): elements sorted by (coordinate, position), cached."""
     torch = _torch()
@@ -802,7 +828,7 @@ def max_row_length(tensor: AltoTensor, mode: int) -> int:
     key = ("maxrun", mode)
     hit = tensor._cache.get(key)
     if hit is None:
-        _perm, ptr = row_index(tensor, mode)
+        ptr = row_ptr(tensor, mode)
         hit = int((ptr[1:] - ptr[:-1]).max().item()) if ptr.numel() > 1 else 0
         tensor._cache[key] = hit
     return hit

@@ -36,11 +36,11 @@ def main():
         res = {"cfg": cfg, "rep": rep}
         _, res["packed_keys_ms"] = timed(lambda: mk.packed_keys(alto))
         for mode in range(len(c.dims)):
-            _, a = timed(lambda: mk.row_index(alto, mode))
+            _, a = timed(lambda: mk.row_ptr(alto, mode))
             _, b = timed(lambda: mk.hot_slots(alto, mode))
             _, d = timed(lambda: mk.hot_plan_ms(alto, mode, c.rank, torch.float32))
             _, e = timed(lambda: mk.mode_stream(alto, mode, rank=c.rank))
-            res[f"mode{mode}"] = {"row_index_ms": round(a, 2), "hot_slots_ms": round(b, 2), "hot_copies_ms": round(d, 2),
+            res[f"mode{mode}"] = {"row_ptr_ms": round(a, 2), "hot_slots_ms": round(b, 2), "hot_copies_ms": round(d, 2),
                                   "mode_stream_ms": round(e, 2)}
         print(json.dumps(res), flush=True)
 
