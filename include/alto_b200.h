@@ -413,6 +413,11 @@ int alto_pull_slice_rows(const alto_layout* lay, const uint64_t* mkeys, int64_t 
  * per-partition partials are combined in ascending partition order — the
  * Buffered stage + pull of mttkrp.py:148-172 (count = 1 gives mttkrp_seq,
  * mttkrp.py:108-117). */
+/* Elements per row of mode `mode` (a histogram of the mode's coordinates):
+ * counts (I_mode,) uint32, zeroed by the caller.  The hot-row plans need only
+ * these (their prefix sum is alto_row_index's row_ptr). */
+int alto_row_counts(const alto_layout* lay, const void* d_tables, const uint64_t* keys, int64_t m, int32_t mode,
+                    uint32_t* counts, void* stream);
 size_t alto_row_index_workspace_bytes(int64_t m, int64_t dim);
 int alto_row_index(const alto_layout* lay, const void* d_tables,
                    const uint64_t* keys, int64_t m, int32_t mode,

@@ -149,6 +149,7 @@ SIGNATURES = [
     ("alto_hot_rows", c_int32, [c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_size_t, c_void_p]),
     ("alto_hot_plan", c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("alto_row_counts", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     ("alto_row_index_workspace_bytes", c_size_t, [c_int64, c_int64]),
     ("alto_row_index", c_int32, [POINTER(CLayout), c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                  c_void_p, c_size_t, c_void_p]),

@@ -117,6 +117,31 @@ __global__ void delinearize_kernel(const __grid_constant__ DevLayout L, const ui
   }
 }
 
+// Elements per row of one mode (the hot-row plans need only these counts): the
+// warp's 32 consecutive ALTO elements mostly share a few rows, so equal rows
+// are grouped with match.any and one lane adds the group's size.
+template <int W>
+__global__ void row_count_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ tab,
+                                 const uint64_t* __restrict__ keys, long long m, int mode,
+                                 unsigned* __restrict__ counts) {
+  extern __shared__ uint64_t s_dec[];
+  copy_to_smem(s_dec, tab + static_cast<long long>(L.dec_off) * W, L.dec_bytes * 256 * W);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long n_round = (m + stride - 1) / stride * stride;  // whole warps stay in the loop together
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+    const bool ok = i < m;
+    unsigned long long row = 0xffffffff00000000ull | static_cast<unsigned>(lane);  // idle lanes: singletons
+    if (ok) {
+      const Key<W> p = decode_packed<W>(s_dec, L.dec_bytes, load_key<W>(keys, i));
+      row = static_cast<unsigned long long>(packed_field<W>(p, L.pack_off[mode], L.bits[mode]));
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, row);
+    if (ok && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(counts + row, static_cast<unsigned>(__popc(peers)));
+  }
+}
+
 // Per-mode maximum coordinate (container validation: a corrupt file must not
 // drive out-of-range factor/output rows).  Warp max, then one atomicMax per
 // warp and mode.
@@ -280,6 +305,31 @@ int alto_delinearize(const alto_layout* lay, const void* d_tables, const uint64_
     delinearize_kernel<2><<<grid, block, smem, s>>>(d, tab, keys, m, mode, o);
   }
   ALTO_LAUNCH_CHECK("alto_delinearize");
+  return ALTO_OK;
+}
+
+int alto_row_counts(const alto_layout* lay, const void* d_tables, const uint64_t* keys, int64_t m, int32_t mode,
+                    uint32_t* counts, void* stream) {
+  const int st = check_layout(lay);
+  if (st) return st;
+  ALTO_REQUIRE(mode >= 0 && mode < lay->order, "mode out of range");
+  ALTO_REQUIRE(m >= 0 && m < (1ll << 32), "row counts support fewer than 2^32 elements");
+  if (m == 0) return ALTO_OK;
+  ALTO_REQUIRE(d_tables && keys && counts, "null argument");
+  const DevLayout d = make_dev_layout(lay);
+  cudaStream_t s = as_stream(stream);
+  const int block = 256;
+  const int grid = grid_for(m, block, kSMs * 8);
+  const size_t smem = static_cast<size_t>(d.dec_bytes) * 256 * d.n_words * sizeof(uint64_t);
+  const auto* tab = static_cast<const uint64_t*>(d_tables);
+  if (d.n_words == 1) {
+    ALTO_CUDA_TRY(cudaFuncSetAttribute(row_count_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    row_count_kernel<1><<<grid, block, smem, s>>>(d, tab, keys, m, mode, counts);
+  } else {
+    ALTO_CUDA_TRY(cudaFuncSetAttribute(row_count_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    row_count_kernel<2><<<grid, block, smem, s>>>(d, tab, keys, m, mode, counts);
+  }
+  ALTO_LAUNCH_CHECK("alto_row_counts");
   return ALTO_OK;
 }
 

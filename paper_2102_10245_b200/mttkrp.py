@@ -771,8 +771,8 @@ def mttkrp_pull(tensor: AltoTensor, fdev: list, mode: int, out=None, out_dtype=N
 
 def row_ptr(tensor: AltoTensor, mode: int):
     """Per-mode row offsets (I_mode + 1,) int64 — the rows' element counts, which is all the
-    hot-row plans need: the row index's if it is cached, else alto_row_index without the
-    permutation (keys-only sort, no 4-byte-per-element array kept)."""
+    hot-row plans need: the row index's if it is cached, else the prefix sum of
+    alto_row_counts (a histogram: no sort, no 4-byte-per-element permutation kept)."""
     torch = _torch()
     hit = tensor._cache.get(("row_index", mode))
     if hit is not None:
@@ -785,12 +785,12 @@ def row_ptr(tensor: AltoTensor, mode: int):
         m = tensor.nnz
         dim = lay.dims[mode]
         dev = tensor.keys.device
-        ptr = torch.empty(dim + 1, dtype=torch.int64, device=dev)
-        ws_bytes = lib.alto_row_index_workspace_bytes(m, dim)
-        ws = torch.empty(max(int(ws_bytes), 8), dtype=torch.uint8, device=dev)
-        _lib.check(lib.alto_row_index(c_layout(lay), device_tables(lay).data_ptr(), tensor.keys.data_ptr(), m, mode,
-                                      None, ptr.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr()),
-                   "alto_row_index(row_ptr)")
+        counts = torch.zeros(max(dim, 1), dtype=torch.int32, device=dev)
+        _lib.check(lib.alto_row_counts(c_layout(lay), device_tables(lay).data_ptr(), tensor.keys.data_ptr(), m, mode,
+                                       counts.data_ptr(), _lib.stream_ptr()), "alto_row_counts")
+        ptr = torch.zeros(dim + 1, dtype=torch.int64, device=dev)
+        # counts are uint32 in an int32 tensor (a row holds fewer than 2^32 elements): widen without sign
+        torch.cumsum(counts[:dim].to(torch.int64) & 0xFFFFFFFF, 0, out=ptr[1:])
         tensor._cache[key] = ptr
     return ptr
 

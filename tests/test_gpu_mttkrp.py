@@ -405,6 +405,25 @@ class TestStreamKernel:
         want = (f32[pa][:, None, :] * f32[pb][None, :, :]).reshape(-1, 16)
         assert np.array_equal(tab.cpu().numpy(), want)
 
+    @pytest.mark.parametrize("cfg,nnz", [(2, 300_001), ("wide", 70_001), (4, 1_000)])
+    def test_row_counts_equal_row_index(self, at, cfg, nnz):
+        """alto_row_counts (histogram) + prefix sum == the row offsets of alto_row_index (sort)."""
+        import importlib
+
+        import torch
+
+        mk = importlib.import_module("paper_2102_10245_b200.mttkrp")
+        st = synth.make_tensor(self.WIDE if cfg == "wide" else cfg, nnz=nnz)
+        dims = st.config.dims
+        alto = at.build_alto(at.CooTensor(dims, st.coords, st.values.astype(np.float64)), dtype="float32")
+        for mode in range(len(dims)):
+            ptr = mk.row_ptr(alto, mode)  # histogram path (no row index cached yet)
+            assert ("row_ptr", mode) in alto._cache
+            ref = mk.row_index(alto, mode)[1]
+            assert torch.equal(ptr, ref)
+            want = np.concatenate([[0], np.cumsum(np.bincount(st.coords[:, mode], minlength=dims[mode]))])
+            assert np.array_equal(ptr.cpu().numpy(), want)
+
     def test_hot_copy_plan(self, at):
         """alto_hot_copies: per hot row 2^lg copies with 2^lg * HOT_BOUND >=
         estimated merges (lg <= HOT_MAX_LG), laid out slot by slot."""
