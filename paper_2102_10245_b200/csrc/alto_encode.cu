@@ -117,28 +117,62 @@ __global__ void delinearize_kernel(const __grid_constant__ DevLayout L, const ui
   }
 }
 
-// Elements per row of one mode (the hot-row plans need only these counts): the
-// warp's 32 consecutive ALTO elements mostly share a few rows, so equal rows
-// are grouped with match.any and one lane adds the group's size.
+// Elements per row of one mode (the hot-row plans need only these counts).  The
+// warp's 32 consecutive ALTO elements mostly share a few rows: equal rows are
+// grouped with match.any and one lane adds the group's size — into a small
+// direct-mapped table of the CTA in shared memory (row -> count; a colliding
+// row evicts the resident one to global memory), so the Zipf-head rows, which
+// every warp sees, reach their global counters once per CTA instead of once
+// per warp instruction (same-address atomics serialise in one L2 slice).
+constexpr int kCountSlots = 1024;
+
 template <int W>
 __global__ void row_count_kernel(const __grid_constant__ DevLayout L, const uint64_t* __restrict__ tab,
                                  const uint64_t* __restrict__ keys, long long m, int mode,
                                  unsigned* __restrict__ counts) {
   extern __shared__ uint64_t s_dec[];
+  __shared__ unsigned long long s_slot[kCountSlots];  // (row + 1) << 32 | count; 0 = empty
   copy_to_smem(s_dec, tab + static_cast<long long>(L.dec_off) * W, L.dec_bytes * 256 * W);
+  for (int i = threadIdx.x; i < kCountSlots; i += blockDim.x) s_slot[i] = 0ull;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  const long long n_round = (m + stride - 1) / stride * stride;  // whole warps stay in the loop together
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
-    const bool ok = i < m;
+  // a CTA walks a contiguous chunk (consecutive ALTO elements share rows)
+  const long long per = (m + gridDim.x - 1) / gridDim.x;
+  const long long lo = blockIdx.x * per, hi = min(m, lo + per);
+  const long long n_round = lo + (hi - lo + blockDim.x - 1) / blockDim.x * blockDim.x;  // whole warps stay together
+  for (long long i = lo + threadIdx.x; i < n_round; i += blockDim.x) {
+    const bool ok = i < hi;
     unsigned long long row = 0xffffffff00000000ull | static_cast<unsigned>(lane);  // idle lanes: singletons
     if (ok) {
       const Key<W> p = decode_packed<W>(s_dec, L.dec_bytes, load_key<W>(keys, i));
       row = static_cast<unsigned long long>(packed_field<W>(p, L.pack_off[mode], L.bits[mode]));
     }
     const unsigned peers = __match_any_sync(0xffffffffu, row);
-    if (ok && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(counts + row, static_cast<unsigned>(__popc(peers)));
+    if (ok && (peers & ((1u << lane) - 1u)) == 0u) {
+      const unsigned add = static_cast<unsigned>(__popc(peers));
+      unsigned long long* slot = s_slot + (static_cast<unsigned>(row) & (kCountSlots - 1));
+      const unsigned long long tag = (row + 1ull) << 32;
+      unsigned long long cur = *slot;
+      while (true) {
+        if ((cur >> 32) == (tag >> 32)) {  // resident: add (count < 2^32 per CTA chunk)
+          const unsigned long long seen = atomicCAS(slot, cur, cur + add);
+          if (seen == cur) break;
+          cur = seen;
+        } else {  // empty or another row: take the slot, flush what was there
+          const unsigned long long seen = atomicCAS(slot, cur, tag | add);
+          if (seen == cur) {
+            if (cur) atomicAdd(counts + ((cur >> 32) - 1ull), static_cast<unsigned>(cur));
+            break;
+          }
+          cur = seen;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCountSlots; i += blockDim.x) {
+    const unsigned long long cur = s_slot[i];
+    if (cur) atomicAdd(counts + ((cur >> 32) - 1ull), static_cast<unsigned>(cur));
   }
 }
 
